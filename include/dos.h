@@ -1,0 +1,172 @@
+/*
+ * dos.h — C ABI of libdos.so, the B200-native Deep Optimizer States update
+ * phase (arXiv 2410.21316).  Plain pointers and sizes only; no torch types.
+ *
+ * Every entry point returns 0 on success or a negative DOS_E* code; the
+ * message for the calling thread is available from dos_last_error().
+ * Error classes mirror the reference's exception types:
+ *   DOS_EINVAL -> ValueError, DOS_ETYPE -> TypeError, DOS_ECUDA/DOS_ESYS ->
+ *   RuntimeError, DOS_EINFEASIBLE -> InfeasibleConfigError.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/pkg/src/optistate):
+ *   dos_adam_step_host / dos_adam_step_cuda
+ *       kernels.py:107-139 adam_step_arrays (validation + scalars in Python,
+ *       the per-element loop here), kernels.py:88-101 _adam_step_jit,
+ *       fused with core.py:201-205 upscale (grad load) and
+ *       core.py:190-198 downscale_rne (working-copy store).
+ *   dos_downscale_host / dos_upscale_host / dos_downscale_cuda / dos_upscale_cuda
+ *       core.py:190-198 downscale_rne, core.py:201-205 upscale,
+ *       executor.py:317-349 flush_gradients (GPU_UPSCALE_FP32 leg).
+ *   dos_host_alloc / dos_host_free
+ *       core.py:208-272 ShardedOptimizer's flat arrays -> a pinned host pool.
+ *   dos_exec_* (the copy-stream / host-lane engine)
+ *       executor.py:174-235 ExecutorTarget.apply (numeric effect per action)
+ *       driven by scheduler.py:402-466 run_update (one submit per action, in
+ *       emission order); executor.py:120-171 EmulatedDevice -> HBM slots.
+ */
+#ifndef DOS_H
+#define DOS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* error codes */
+#define DOS_OK 0
+#define DOS_EINVAL (-1)
+#define DOS_ETYPE (-2)
+#define DOS_ECUDA (-3)
+#define DOS_ESYS (-4)
+#define DOS_EINFEASIBLE (-5)
+#define DOS_ESTATE (-6) /* structural violation (double stage, missing triplet, ...) */
+
+/* element dtypes */
+#define DOS_NONE (-1)
+#define DOS_F32 0
+#define DOS_F16 1
+#define DOS_BF16 2
+
+/* Per-step scalars, prepared by the caller exactly as kernels.py:122-135:
+ * bc1/bc2 = f32(1 - pow(beta, step)) in double, lr/betas/eps cast to f32.
+ * (1 - beta) is formed on the device/host as the fp32 difference 1.0f - beta.
+ * adamw != 0 applies decoupled weight decay p = p * (1 - lr*wd) before the
+ * Adam step (no reference pin: the reference has no weight decay). */
+typedef struct dos_adam_scalars {
+  float lr, beta1, beta2, eps, bc1, bc2, weight_decay;
+  int32_t adamw;
+} dos_adam_scalars;
+
+const char* dos_last_error(void);
+int dos_version(void);
+
+/* ---- K1: fused Adam on the GPU (sm_100a).  Asynchronous on `stream`
+ * (a cudaStream_t; NULL = legacy default).  p/m/v fp32 in place; g in
+ * g_dtype (F32/F16/BF16); if lowp_dtype != DOS_NONE the updated params are
+ * also written to p_lowp in that dtype (RNE) in the same pass. */
+int dos_adam_step_cuda(float* p, float* m, float* v, const void* g, int g_dtype,
+                       void* p_lowp, int lowp_dtype, int64_t n,
+                       const dos_adam_scalars* s, void* stream);
+
+/* ---- H1: the same update on host cores (bit-identical results).  Blocks
+ * the calling thread only; nthreads <= 0 uses the library's host team. */
+int dos_adam_step_host(float* p, float* m, float* v, const void* g, int g_dtype,
+                       void* p_lowp, int lowp_dtype, int64_t n,
+                       const dos_adam_scalars* s, int nthreads);
+
+/* ---- conversions (numpy-exact fp16 incl. NaN payloads; torch-exact bf16) */
+int dos_downscale_host(const float* x, void* out, int out_dtype, int64_t n, int nthreads);
+int dos_upscale_host(const void* x, int in_dtype, float* out, int64_t n, int nthreads);
+int dos_downscale_cuda(const float* x, void* out, int out_dtype, int64_t n, void* stream);
+int dos_upscale_cuda(const void* x, int in_dtype, float* out, int64_t n, void* stream);
+
+/* ---- host pool: page-aligned, THP-advised, first-touched by the host
+ * team, then page-locked and registered with CUDA (if a device is present
+ * and register_cuda != 0).  numa_node < 0: no binding. */
+int dos_host_alloc(size_t bytes, int numa_node, int register_cuda, void** out);
+int dos_host_free(void* ptr);
+int dos_host_threads(void); /* size of the library's host team */
+int dos_set_host_threads(int n);
+
+/* ---- the copy-stream / host-lane engine ---------------------------------
+ * Action kinds and lanes use the reference's enum order
+ * (scheduler.py:43-89). */
+enum dos_action_kind {
+  DOS_CPU_UPDATE = 0,
+  DOS_GPU_UPDATE = 1,
+  DOS_CPU_DOWNSCALE = 2,
+  DOS_H2D_PARAMS16 = 3,
+  DOS_FLUSH_OUT_MODEL16 = 4,
+  DOS_FLUSH_OUT_M = 5,
+  DOS_FLUSH_OUT_V = 6,
+  DOS_FLUSH_OUT_P = 7,
+  DOS_PREFETCH_M = 8,
+  DOS_PREFETCH_V = 9,
+  DOS_PREFETCH_P = 10,
+  DOS_GRAD_FLUSH = 11
+};
+enum dos_lane { DOS_LANE_CPU = 0, DOS_LANE_FAST = 1, DOS_LANE_H2D = 2, DOS_LANE_D2H = 3 };
+
+/* Where one rank's state lives.  Host arrays are indexed by the flat shard
+ * offset; device static-resident state is compact (static_offset[i] gives the
+ * element offset of subgroup i in dev_static_{p,m,v}, -1 if not static). */
+typedef struct dos_state_desc {
+  int32_t num_subgroups;
+  const int64_t* sg_start; /* [num_subgroups] */
+  const int64_t* sg_size;  /* [num_subgroups] */
+  const int64_t* static_offset; /* [num_subgroups], -1 = not resident */
+  int32_t lowp_dtype;      /* DOS_F16 or DOS_BF16: grads and working copy */
+  /* host (pinned) */
+  float* host_p;
+  float* host_m;
+  float* host_v;
+  const void* host_g;      /* lowp grads for CPU subgroups (flushed before the phase) */
+  void* host_lowp;         /* staging for CPU-downscaled params (H2D_PARAMS16 source) */
+  /* device (HBM) */
+  const void* dev_g;       /* lowp grads, whole shard */
+  void* dev_lowp;          /* working copy, whole shard */
+  float* dev_static_p;
+  float* dev_static_m;
+  float* dev_static_v;
+} dos_state_desc;
+
+typedef struct dos_exec_config {
+  int32_t device;
+  int32_t num_slots;      /* physical HBM windows (1 or 2) */
+  int64_t slot_elems;     /* elements per slot piece (>= largest dynamic subgroup) */
+  int32_t host_threads;   /* <=0: library default team */
+  int32_t fuse_downscale; /* !=0: CPU_UPDATE writes host_lowp; CPU_DOWNSCALE is a marker */
+} dos_exec_config;
+
+typedef struct dos_action_desc {
+  int32_t id;
+  int32_t kind;
+  int32_t subgroup;     /* -1 for batched CPU_DOWNSCALE */
+  int32_t lane;
+  int32_t is_static;    /* the subgroup is fast-tier resident */
+  int32_t num_deps;
+  const int32_t* deps;
+  int32_t batch_len;
+  const int32_t* batch;
+} dos_action_desc;
+
+int dos_exec_create(const dos_exec_config* cfg, void** out);
+int dos_exec_destroy(void* ex);
+/* Start a phase: binds state + scalars, records the t0 marker.  max_actions
+ * bounds the action ids of this phase. */
+int dos_exec_begin(void* ex, const dos_state_desc* st, const dos_adam_scalars* s,
+                   int32_t max_actions);
+/* Enqueue one action (never waits on the GPU or the host lane). */
+int dos_exec_submit(void* ex, const dos_action_desc* a);
+/* Wait for the phase; fills measured [start,end) in ns since t0 per action id
+ * (arrays of length >= number of submitted actions). */
+int dos_exec_finish(void* ex, int64_t* start_ns, int64_t* end_ns, int32_t n);
+/* Device pointer of a staging slot piece (0=m,1=v,2=p) for tests/inspection. */
+int dos_exec_slot_ptr(void* ex, int32_t slot, int32_t piece, float** out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DOS_H */

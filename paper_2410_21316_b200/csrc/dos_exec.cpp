@@ -1,0 +1,526 @@
+// dos_exec.cpp — the copy-stream / host-lane engine of the update phase.
+//
+// The reference executes a plan by calling ExecutorTarget.apply once per
+// action in emission order from one thread (scheduler.py:402-466 run_update,
+// executor.py:192-235 apply), with numpy copies standing in for the fast
+// tier (executor.py:120-171 EmulatedDevice).  Here each submit() *enqueues*
+// the action's real effect and returns immediately:
+//
+//   lane FAST_COMPUTE -> CUDA stream `fast`  (K1; FLUSH_OUT_MODEL16 is fused
+//                                             into K1's working-copy store)
+//   lane H2D          -> CUDA stream `h2d`   (pinned cudaMemcpyAsync)
+//   lane D2H          -> CUDA stream `d2h`   (pinned cudaMemcpyAsync)
+//   lane CPU_COMPUTE  -> one host worker thread driving the H1 team
+//
+// Each lane is FIFO in emission order, exactly the reference's lane model.
+// Dependencies: GPU->GPU by cudaStreamWaitEvent; host->GPU by
+// cuStreamWaitValue32 on a per-action flag in mapped pinned memory (the host
+// worker writes the phase epoch when the action ends), so the dispatcher
+// never blocks; GPU->host by cudaEventSynchronize in the worker.  Emission
+// order is topological and every lane serves it in order, so no wait can
+// deadlock.
+//
+// Staging (Alg. 1's p_tmp/m_tmp/v_tmp): `num_slots` HBM
+// windows of {m, v, p}.  A window is taken at PREFETCH_M and released by the
+// last of its flushes; a new window waits for that flush's end event.  This
+// physically double-buffers what the reference models as one staging buffer
+// per state stream, so the next subgroup's prefetch overlaps the current
+// update and flush (the plan itself is unchanged).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <string.h>
+
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "dos_internal.h"
+
+namespace {
+
+typedef CUresult (*pfn_wait_value32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+int64_t now_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+#define DOS_CU(call)                                                                                       \
+  do {                                                                                                     \
+    cudaError_t e__ = (call);                                                                              \
+    if (e__ != cudaSuccess) return dos_set_error(DOS_ECUDA, "%s failed: %s", #call, cudaGetErrorString(e__)); \
+  } while (0)
+
+enum { PIECE_M = 0, PIECE_V = 1, PIECE_P = 2 };
+
+struct Job {
+  int32_t id, kind, sg;
+  std::vector<int32_t> deps, batch;
+};
+
+struct Engine {
+  int dev = 0;
+  cudaStream_t st[3] = {nullptr, nullptr, nullptr};  // fast, h2d, d2h
+  int nslots = 0;
+  int64_t slot_elems = 0;
+  float* slot_mem = nullptr;
+  bool fuse = true;
+  int host_threads = 0;
+
+  // phase
+  bool active = false;
+  dos_state_desc S{};
+  std::vector<int64_t> sg_start, sg_size, static_off;
+  dos_kscal K{};
+  int32_t max_actions = 0, count = 0;
+  std::vector<cudaEvent_t> ev_s, ev_e;
+  cudaEvent_t ev0 = nullptr;
+  std::vector<uint8_t> is_host;
+  std::vector<int64_t> host_s, host_e;
+  uint32_t* flags = nullptr;  // mapped pinned
+  CUdeviceptr flags_dev = 0;
+  int32_t flags_cap = 0;
+  uint32_t epoch = 0;
+  pfn_wait_value32 wait_fn = nullptr;
+  bool wait_value_ok = true;
+  int64_t host_t0 = 0;
+
+  // staging bookkeeping
+  std::vector<int> sg_slot;
+  std::vector<uint8_t> sg_mask;
+  int next_slot = 0;
+  int slot_release[2] = {-1, -1};  // action id whose end frees the slot; -2 = window open
+  int slot_owner[2] = {-1, -1};
+
+  // dispatcher error (first one wins)
+  int err = DOS_OK;
+  std::string errmsg;
+
+  // host lane
+  std::thread worker;
+  std::mutex mu;
+  std::condition_variable cv, done_cv;
+  std::deque<Job> q;
+  bool stop = false;
+  int inflight = 0;
+  std::vector<uint8_t> host_done;
+  int host_err = DOS_OK;
+  std::string host_errmsg;
+
+  float* slot_ptr(int s, int piece) { return slot_mem + ((int64_t)s * 3 + piece) * slot_elems; }
+
+  int fail(int code, const std::string& msg) {
+    if (err == DOS_OK) {
+      err = code;
+      errmsg = msg;
+    }
+    return dos_set_error(code, "%s", msg.c_str());
+  }
+
+  // ---- host worker
+  void worker_loop() {
+    cudaSetDevice(dev);
+    for (;;) {
+      Job j;
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return stop || !q.empty(); });
+        if (q.empty()) return;
+        j = std::move(q.front());
+        q.pop_front();
+      }
+      int rc = DOS_OK;
+      std::string msg;
+      for (int32_t d : j.deps) {
+        if (!is_host[d]) {
+          cudaError_t e = cudaEventSynchronize(ev_e[d]);
+          if (e != cudaSuccess && rc == DOS_OK) {
+            rc = DOS_ECUDA;
+            msg = std::string("waiting on GPU dep failed: ") + cudaGetErrorString(e);
+          }
+        }
+      }
+      const int64_t t_s = now_ns();
+      if (rc == DOS_OK) rc = run_host(j, msg);
+      const int64_t t_e = now_ns();
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        host_s[j.id] = t_s - host_t0;
+        host_e[j.id] = t_e - host_t0;
+        host_done[j.id] = 1;
+        if (rc != DOS_OK && host_err == DOS_OK) {
+          host_err = rc;
+          host_errmsg = msg;
+        }
+        --inflight;
+      }
+      __atomic_store_n(&flags[j.id], epoch, __ATOMIC_RELEASE);
+      done_cv.notify_all();
+    }
+  }
+
+  int run_host(const Job& j, std::string& msg) {
+    const int lt = S.lowp_dtype;
+    if (j.kind == DOS_CPU_UPDATE) {
+      const int64_t a = sg_start[j.sg], n = sg_size[j.sg];
+      const void* g = static_cast<const char*>(S.host_g) + 2 * a;
+      void* lp = fuse ? static_cast<void*>(static_cast<char*>(S.host_lowp) + 2 * a) : nullptr;
+      const int rc = dos_host_adam(S.host_p + a, S.host_m + a, S.host_v + a, g, lt, lp, fuse ? lt : DOS_NONE, n, K,
+                                   host_threads);
+      if (rc != DOS_OK) msg = dos_last_error();
+      return rc;
+    }
+    if (j.kind == DOS_CPU_DOWNSCALE) {
+      if (fuse) return DOS_OK;  // already written by the fused CPU_UPDATE
+      for (int32_t b : j.batch) {
+        const int64_t a = sg_start[b], n = sg_size[b];
+        const int rc = dos_host_down(S.host_p + a, static_cast<char*>(S.host_lowp) + 2 * a, lt, n, host_threads);
+        if (rc != DOS_OK) {
+          msg = dos_last_error();
+          return rc;
+        }
+      }
+      return DOS_OK;
+    }
+    msg = "action kind " + std::to_string(j.kind) + " is not a host-lane action";
+    return DOS_EINVAL;
+  }
+
+  void wait_host_action(int32_t id) {
+    std::unique_lock<std::mutex> lk(mu);
+    done_cv.wait(lk, [&] { return host_done[id] != 0; });
+  }
+
+  // ---- GPU dependency edges
+  int gpu_wait_deps(cudaStream_t s, const dos_action_desc* a) {
+    for (int k = 0; k < a->num_deps; ++k) {
+      const int32_t d = a->deps[k];
+      if (is_host[d]) {
+        bool done = false;
+        if (wait_value_ok && wait_fn) {
+          CUresult r = wait_fn((CUstream)s, flags_dev + 4 * (CUdeviceptr)d, epoch, CU_STREAM_WAIT_VALUE_GEQ);
+          if (r == CUDA_SUCCESS) done = true;
+          else wait_value_ok = false;  // fall back to blocking the dispatcher
+        }
+        if (!done) wait_host_action(d);
+      } else {
+        DOS_CU(cudaStreamWaitEvent(s, ev_e[d], 0));
+      }
+    }
+    return DOS_OK;
+  }
+
+  int submit(const dos_action_desc* a) {
+    if (!active) return fail(DOS_ESTATE, "dos_exec_submit outside a phase");
+    if (a->id != count || a->id >= max_actions)
+      return fail(DOS_EINVAL, "action id " + std::to_string(a->id) + " out of emission order (expected " +
+                                  std::to_string(count) + ")");
+    for (int k = 0; k < a->num_deps; ++k)
+      if (a->deps[k] < 0 || a->deps[k] >= a->id)
+        return fail(DOS_EINVAL, "action " + std::to_string(a->id) + " has a forward dependency");
+    const int sg = a->subgroup;
+    if (a->kind != DOS_CPU_DOWNSCALE && (sg < 0 || sg >= S.num_subgroups))
+      return fail(DOS_EINVAL, "action " + std::to_string(a->id) + " names subgroup " + std::to_string(sg));
+    ++count;
+
+    if (a->lane == DOS_LANE_CPU) {
+      is_host[a->id] = 1;
+      Job j;
+      j.id = a->id;
+      j.kind = a->kind;
+      j.sg = sg;
+      j.deps.assign(a->deps, a->deps + a->num_deps);
+      j.batch.assign(a->batch, a->batch + a->batch_len);
+      for (int32_t b : j.batch)
+        if (b < 0 || b >= S.num_subgroups) return fail(DOS_EINVAL, "downscale batch names a bad subgroup");
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        q.push_back(std::move(j));
+        ++inflight;
+      }
+      cv.notify_one();
+      return DOS_OK;
+    }
+
+    cudaStream_t s = a->lane == DOS_LANE_FAST ? st[0] : a->lane == DOS_LANE_H2D ? st[1] : st[2];
+    int rc = gpu_wait_deps(s, a);
+    if (rc != DOS_OK) return fail(rc, dos_last_error());
+    DOS_CU(cudaEventRecord(ev_s[a->id], s));
+    rc = enqueue_gpu(a, s);
+    if (rc != DOS_OK) return fail(rc, dos_last_error());
+    DOS_CU(cudaEventRecord(ev_e[a->id], s));
+    return DOS_OK;
+  }
+
+  int enqueue_gpu(const dos_action_desc* a, cudaStream_t s) {
+    const int sg = a->subgroup;
+    const int64_t start = sg_start[sg], n = sg_size[sg];
+    const int lt = S.lowp_dtype;
+    char* dev_lowp = static_cast<char*>(S.dev_lowp);
+    const char* dev_g = static_cast<const char*>(S.dev_g);
+    switch (a->kind) {
+      case DOS_PREFETCH_M:
+      case DOS_PREFETCH_V:
+      case DOS_PREFETCH_P: {
+        if (a->is_static) return dos_set_error(DOS_ESTATE, "static subgroup %d prefetched", sg);
+        const int piece = a->kind == DOS_PREFETCH_M ? PIECE_M : a->kind == DOS_PREFETCH_V ? PIECE_V : PIECE_P;
+        if (n > slot_elems) return dos_set_error(DOS_EINFEASIBLE, "subgroup %d (%lld) exceeds the HBM window", sg, (long long)n);
+        if (sg_slot[sg] < 0) {
+          // window opens: take the next physical slot
+          const int sl = next_slot;
+          if (slot_release[sl] == -2)
+            return dos_set_error(DOS_EINFEASIBLE,
+                                 "subgroup %d opens a window while slot %d (subgroup %d) is still unflushed", sg, sl,
+                                 slot_owner[sl]);
+          if (slot_release[sl] >= 0) DOS_CU(cudaStreamWaitEvent(s, ev_e[slot_release[sl]], 0));
+          next_slot = (sl + 1) % nslots;
+          slot_release[sl] = -2;
+          slot_owner[sl] = sg;
+          sg_slot[sg] = sl;
+        }
+        if (sg_mask[sg] & (1u << piece))
+          return dos_set_error(DOS_ESTATE, "subgroup %d piece %c staged twice", sg, "mvp"[piece]);
+        sg_mask[sg] |= (uint8_t)(1u << piece);
+        const float* src = (piece == PIECE_M ? S.host_m : piece == PIECE_V ? S.host_v : S.host_p) + start;
+        DOS_CU(cudaMemcpyAsync(slot_ptr(sg_slot[sg], piece), src, (size_t)n * 4, cudaMemcpyHostToDevice, s));
+        return DOS_OK;
+      }
+      case DOS_GPU_UPDATE: {
+        const void* g = dev_g + 2 * start;
+        void* lp = dev_lowp + 2 * start;
+        if (a->is_static) {
+          const int64_t o = static_off[sg];
+          if (o < 0) return dos_set_error(DOS_ESTATE, "subgroup %d marked static but has no HBM residence", sg);
+          return dos_adam_launch(S.dev_static_p + o, S.dev_static_m + o, S.dev_static_v + o, g, lt, lp, lt, n, K, s);
+        }
+        if (sg_slot[sg] < 0 || sg_mask[sg] != 7u)
+          return dos_set_error(DOS_ESTATE, "fast update of subgroup %d with missing pieces (mask %u)", sg,
+                               (unsigned)sg_mask[sg]);
+        const int sl = sg_slot[sg];
+        return dos_adam_launch(slot_ptr(sl, PIECE_P), slot_ptr(sl, PIECE_M), slot_ptr(sl, PIECE_V), g, lt, lp, lt, n,
+                               K, s);
+      }
+      case DOS_FLUSH_OUT_MODEL16:
+        // K1 already stored the working copy in the same pass.
+        if (!a->is_static && !(sg_slot[sg] >= 0 && (sg_mask[sg] & (1u << PIECE_P))))
+          return dos_set_error(DOS_ESTATE, "FLUSH_OUT_MODEL16 of subgroup %d without staged params", sg);
+        return DOS_OK;
+      case DOS_FLUSH_OUT_M:
+      case DOS_FLUSH_OUT_V:
+      case DOS_FLUSH_OUT_P: {
+        const int piece = a->kind == DOS_FLUSH_OUT_M ? PIECE_M : a->kind == DOS_FLUSH_OUT_V ? PIECE_V : PIECE_P;
+        if (sg_slot[sg] < 0 || !(sg_mask[sg] & (1u << piece)))
+          return dos_set_error(DOS_ESTATE, "subgroup %d piece %c not resident on device", sg, "mvp"[piece]);
+        float* dst = (piece == PIECE_M ? S.host_m : piece == PIECE_V ? S.host_v : S.host_p) + start;
+        const int sl = sg_slot[sg];
+        DOS_CU(cudaMemcpyAsync(dst, slot_ptr(sl, piece), (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+        sg_mask[sg] &= (uint8_t)~(1u << piece);
+        if (sg_mask[sg] == 0) {  // window closes with this flush
+          slot_release[sl] = a->id;
+          sg_slot[sg] = -1;
+        }
+        return DOS_OK;
+      }
+      case DOS_H2D_PARAMS16:
+        DOS_CU(cudaMemcpyAsync(dev_lowp + 2 * start, static_cast<const char*>(S.host_lowp) + 2 * start, (size_t)n * 2,
+                               cudaMemcpyHostToDevice, s));
+        return DOS_OK;
+      default:
+        return dos_set_error(DOS_EINVAL, "unexpected action kind %d on a device lane", a->kind);
+    }
+  }
+
+  int begin(const dos_state_desc* st_desc, const dos_adam_scalars* sc, int32_t nmax) {
+    if (active) return dos_set_error(DOS_ESTATE, "a phase is already active");
+    if (!st_desc || !sc) return dos_set_error(DOS_EINVAL, "NULL state or scalars");
+    if (st_desc->lowp_dtype != DOS_F16 && st_desc->lowp_dtype != DOS_BF16)
+      return dos_set_error(DOS_ETYPE, "working-copy dtype %d unsupported", st_desc->lowp_dtype);
+    if (nmax < 0) return dos_set_error(DOS_EINVAL, "max_actions must be >= 0");
+    DOS_CU(cudaSetDevice(dev));
+    S = *st_desc;
+    const int ns = S.num_subgroups;
+    sg_start.assign(S.sg_start, S.sg_start + ns);
+    sg_size.assign(S.sg_size, S.sg_size + ns);
+    if (S.static_offset) static_off.assign(S.static_offset, S.static_offset + ns);
+    else static_off.assign(ns, -1);
+    K = dos_make_kscal(sc);
+    const int32_t cap = nmax > 0 ? nmax : 1;
+    while ((int32_t)ev_s.size() < cap) {
+      cudaEvent_t a, b;
+      DOS_CU(cudaEventCreate(&a));
+      DOS_CU(cudaEventCreate(&b));
+      ev_s.push_back(a);
+      ev_e.push_back(b);
+    }
+    if (flags_cap < cap) {
+      if (flags) cudaFreeHost(flags);
+      flags = nullptr;
+      int32_t want = std::max(cap, 1024);
+      DOS_CU(cudaHostAlloc(reinterpret_cast<void**>(&flags), (size_t)want * 4, cudaHostAllocMapped));
+      memset(flags, 0, (size_t)want * 4);
+      void* dptr = nullptr;
+      DOS_CU(cudaHostGetDevicePointer(&dptr, flags, 0));
+      flags_dev = (CUdeviceptr)dptr;
+      flags_cap = want;
+      epoch = 0;
+    }
+    ++epoch;
+    if (epoch == 0) {  // wrapped: reset
+      memset(flags, 0, (size_t)flags_cap * 4);
+      epoch = 1;
+    }
+    max_actions = cap;
+    count = 0;
+    is_host.assign(cap, 0);
+    host_done.assign(cap, 0);
+    host_s.assign(cap, 0);
+    host_e.assign(cap, 0);
+    sg_slot.assign(ns, -1);
+    sg_mask.assign(ns, 0);
+    next_slot = 0;
+    slot_release[0] = slot_release[1] = -1;
+    slot_owner[0] = slot_owner[1] = -1;
+    err = DOS_OK;
+    errmsg.clear();
+    host_err = DOS_OK;
+    host_errmsg.clear();
+    DOS_CU(cudaEventRecord(ev0, st[0]));
+    DOS_CU(cudaStreamWaitEvent(st[1], ev0, 0));
+    DOS_CU(cudaStreamWaitEvent(st[2], ev0, 0));
+    DOS_CU(cudaEventSynchronize(ev0));
+    host_t0 = now_ns();
+    active = true;
+    return DOS_OK;
+  }
+
+  int finish(int64_t* start_ns, int64_t* end_ns, int32_t n) {
+    if (!active) return dos_set_error(DOS_ESTATE, "dos_exec_finish without an active phase");
+    {
+      std::unique_lock<std::mutex> lk(mu);
+      done_cv.wait(lk, [&] { return inflight == 0; });
+    }
+    active = false;
+    cudaError_t ce = cudaSuccess;
+    for (int i = 0; i < 3; ++i) {
+      cudaError_t e = cudaStreamSynchronize(st[i]);
+      if (e != cudaSuccess && ce == cudaSuccess) ce = e;
+    }
+    if (ce != cudaSuccess) return dos_set_error(DOS_ECUDA, "update phase failed on the device: %s", cudaGetErrorString(ce));
+    if (host_err != DOS_OK) return dos_set_error(host_err, "host lane: %s", host_errmsg.c_str());
+    if (err != DOS_OK) return dos_set_error(err, "%s", errmsg.c_str());
+    for (int i = 0; i < 2; ++i)
+      if (slot_release[i] == -2)
+        return dos_set_error(DOS_ESTATE, "staging store not drained: subgroup %d", slot_owner[i]);
+    const int32_t k = std::min(n, count);
+    for (int32_t i = 0; i < k; ++i) {
+      if (is_host[i]) {
+        start_ns[i] = host_s[i];
+        end_ns[i] = host_e[i];
+      } else {
+        float ms_s = 0.f, ms_e = 0.f;
+        DOS_CU(cudaEventElapsedTime(&ms_s, ev0, ev_s[i]));
+        DOS_CU(cudaEventElapsedTime(&ms_e, ev0, ev_e[i]));
+        start_ns[i] = (int64_t)((double)ms_s * 1e6);
+        end_ns[i] = (int64_t)((double)ms_e * 1e6);
+      }
+    }
+    return DOS_OK;
+  }
+
+  int create(const dos_exec_config* c) {
+    dev = c->device;
+    nslots = c->num_slots;
+    slot_elems = c->slot_elems;
+    fuse = c->fuse_downscale != 0;
+    host_threads = c->host_threads;
+    if (nslots < 1 || nslots > 2) return dos_set_error(DOS_EINVAL, "num_slots must be 1 or 2");
+    if (slot_elems < 0) return dos_set_error(DOS_EINVAL, "slot_elems must be >= 0");
+    DOS_CU(cudaSetDevice(dev));
+    for (int i = 0; i < 3; ++i) DOS_CU(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking));
+    DOS_CU(cudaEventCreate(&ev0));
+    if (slot_elems > 0) DOS_CU(cudaMalloc(reinterpret_cast<void**>(&slot_mem), (size_t)nslots * 3 * slot_elems * 4));
+    cudaDriverEntryPointQueryResult qr;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      wait_fn = reinterpret_cast<pfn_wait_value32>(fn);
+    else
+      cudaGetLastError();
+    worker = std::thread([this] { worker_loop(); });
+    return DOS_OK;
+  }
+
+  void destroy() {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      stop = true;
+    }
+    cv.notify_all();
+    if (worker.joinable()) worker.join();
+    cudaSetDevice(dev);
+    for (int i = 0; i < 3; ++i)
+      if (st[i]) {
+        cudaStreamSynchronize(st[i]);
+        cudaStreamDestroy(st[i]);
+      }
+    for (auto e : ev_s) cudaEventDestroy(e);
+    for (auto e : ev_e) cudaEventDestroy(e);
+    if (ev0) cudaEventDestroy(ev0);
+    if (slot_mem) cudaFree(slot_mem);
+    if (flags) cudaFreeHost(flags);
+  }
+};
+
+}  // namespace
+
+extern "C" int dos_exec_create(const dos_exec_config* cfg, void** out) {
+  if (!cfg || !out) return dos_set_error(DOS_EINVAL, "NULL config or out");
+  *out = nullptr;
+  Engine* e = new Engine();
+  const int rc = e->create(cfg);
+  if (rc != DOS_OK) {
+    std::string msg = dos_last_error();
+    e->destroy();
+    delete e;
+    return dos_set_error(rc, "%s", msg.c_str());
+  }
+  *out = e;
+  return DOS_OK;
+}
+
+extern "C" int dos_exec_destroy(void* ex) {
+  if (!ex) return DOS_OK;
+  Engine* e = static_cast<Engine*>(ex);
+  e->destroy();
+  delete e;
+  return DOS_OK;
+}
+
+extern "C" int dos_exec_begin(void* ex, const dos_state_desc* st, const dos_adam_scalars* s, int32_t max_actions) {
+  if (!ex) return dos_set_error(DOS_EINVAL, "NULL engine");
+  return static_cast<Engine*>(ex)->begin(st, s, max_actions);
+}
+
+extern "C" int dos_exec_submit(void* ex, const dos_action_desc* a) {
+  if (!ex || !a) return dos_set_error(DOS_EINVAL, "NULL engine or action");
+  return static_cast<Engine*>(ex)->submit(a);
+}
+
+extern "C" int dos_exec_finish(void* ex, int64_t* start_ns, int64_t* end_ns, int32_t n) {
+  if (!ex) return dos_set_error(DOS_EINVAL, "NULL engine");
+  if (n > 0 && (!start_ns || !end_ns)) return dos_set_error(DOS_EINVAL, "NULL output arrays");
+  return static_cast<Engine*>(ex)->finish(start_ns, end_ns, n);
+}
+
+extern "C" int dos_exec_slot_ptr(void* ex, int32_t slot, int32_t piece, float** out) {
+  if (!ex || !out) return dos_set_error(DOS_EINVAL, "NULL engine or out");
+  Engine* e = static_cast<Engine*>(ex);
+  if (slot < 0 || slot >= e->nslots || piece < 0 || piece > 2) return dos_set_error(DOS_EINVAL, "bad slot/piece");
+  *out = e->slot_ptr(slot, piece);
+  return DOS_OK;
+}

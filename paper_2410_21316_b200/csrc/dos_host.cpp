@@ -1,0 +1,321 @@
+// dos_host.cpp — host side of libdos: error reporting, the host thread team,
+// H1 entry points (bit-exact host Adam + conversions) and the pinned pool.
+//
+// H1 replaces the reference's CPU-lane work:
+//   CPU_UPDATE   -> adam_step_subgroup (pkg/src/optistate/executor.py:77-100)
+//                   = upscale (core.py:201-205) + adam_step_arrays (kernels.py:107-139)
+//   CPU_DOWNSCALE-> downscale_rne per batch member (executor.py:228-231)
+// The reference runs these single-threaded under the GIL (numba @njit without
+// parallel/nogil, kernels.py:90); here a team of pinned threads splits each
+// subgroup into contiguous, cache-line aligned chunks.
+#include <errno.h>
+#include <sched.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "dos_internal.h"
+
+// ---------------------------------------------------------------- errors
+static thread_local std::string g_err;
+
+int dos_set_error(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+extern "C" const char* dos_last_error(void) { return g_err.c_str(); }
+extern "C" int dos_version(void) { return 1; }
+
+// ---------------------------------------------------------------- ISA pick
+static const dos_hk_table& hk() {
+  static const dos_hk_table* t = [] {
+    __builtin_cpu_init();
+    if (__builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw") &&
+        __builtin_cpu_supports("avx512vl") && __builtin_cpu_supports("avx512dq"))
+      return &dos_hk_avx512;
+    if (__builtin_cpu_supports("avx2")) return &dos_hk_avx2;
+    return &dos_hk_generic;
+  }();
+  return *t;
+}
+
+// ---------------------------------------------------------------- team
+// Fork-join pool: thread 0 is the caller; workers 1..n-1 are pinned to the
+// process's allowed CPUs (one per core) and sleep between jobs.
+namespace {
+class Team {
+ public:
+  explicit Team(int n) : n_(std::max(1, n)) {
+    cpu_set_t allowed;
+    CPU_ZERO(&allowed);
+    std::vector<int> cpus;
+    if (sched_getaffinity(0, sizeof allowed, &allowed) == 0)
+      for (int c = 0; c < CPU_SETSIZE; ++c)
+        if (CPU_ISSET(c, &allowed)) cpus.push_back(c);
+    for (int t = 1; t < n_; ++t) {
+      threads_.emplace_back([this, t] { loop(t); });
+      if (!cpus.empty()) {
+        cpu_set_t one;
+        CPU_ZERO(&one);
+        CPU_SET(cpus[t % cpus.size()], &one);
+        pthread_setaffinity_np(threads_.back().native_handle(), sizeof one, &one);
+      }
+    }
+  }
+  ~Team() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& th : threads_) th.join();
+  }
+  int size() const { return n_; }
+  // Runs f(t) for t in [0, k) (k <= size) and waits; serialised across callers.
+  void run(int k, const std::function<void(int)>& f) {
+    std::lock_guard<std::mutex> serial(run_mu_);
+    k = std::max(1, std::min(k, n_));
+    if (k == 1) {
+      f(0);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = &f;
+      active_ = k;
+      pending_ = k - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    f(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [this] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void loop(int t) {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int)>* job;
+      int active;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+        job = job_;
+        active = active_;
+      }
+      if (job && t < active) {
+        (*job)(t);
+        std::lock_guard<std::mutex> lk(mu_);
+        if (--pending_ == 0) done_cv_.notify_one();
+      }
+    }
+  }
+  int n_;
+  std::vector<std::thread> threads_;
+  std::mutex mu_, run_mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* job_ = nullptr;
+  int active_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+std::mutex g_team_mu;
+Team* g_team = nullptr;
+int g_team_want = 0;
+
+int default_threads() {
+  cpu_set_t allowed;
+  CPU_ZERO(&allowed);
+  if (sched_getaffinity(0, sizeof allowed, &allowed) == 0) return std::max(1, CPU_COUNT(&allowed));
+  return std::max(1, (int)std::thread::hardware_concurrency());
+}
+
+Team& team() {
+  std::lock_guard<std::mutex> lk(g_team_mu);
+  if (!g_team) g_team = new Team(g_team_want > 0 ? g_team_want : default_threads());
+  return *g_team;
+}
+
+// Splits [0, n) into k chunks aligned to 64 elements (256 B of fp32).
+template <class F>
+void parallel_chunks(int64_t n, int nthreads, F&& body) {
+  Team& tm = team();
+  int k = nthreads > 0 ? std::min(nthreads, tm.size()) : tm.size();
+  const int64_t min_chunk = 1 << 16;  // below this, threading costs more than it saves
+  k = (int)std::max<int64_t>(1, std::min<int64_t>(k, (n + min_chunk - 1) / min_chunk));
+  if (k <= 1) {
+    body((int64_t)0, n);
+    return;
+  }
+  const int64_t per = ((n + k - 1) / k + 63) & ~int64_t(63);
+  tm.run(k, [&](int t) {
+    const int64_t lo = std::min<int64_t>(n, per * t), hi = std::min<int64_t>(n, lo + per);
+    if (lo < hi) body(lo, hi);
+  });
+}
+}  // namespace
+
+extern "C" int dos_host_threads(void) { return team().size(); }
+
+extern "C" int dos_set_host_threads(int n) {
+  std::lock_guard<std::mutex> lk(g_team_mu);
+  g_team_want = n;
+  if (g_team && g_team->size() != (n > 0 ? n : default_threads())) {
+    delete g_team;
+    g_team = nullptr;
+  }
+  return DOS_OK;
+}
+
+// ---------------------------------------------------------------- H1
+int dos_host_adam(float* p, float* m, float* v, const void* g, int gt, void* lp, int lt, int64_t n,
+                  const dos_kscal& s, int nthreads) {
+  const dos_hk_table& t = hk();
+  parallel_chunks(n, nthreads, [&](int64_t lo, int64_t hi) { t.adam(p, m, v, g, gt, lp, lt, lo, hi, s); });
+  return DOS_OK;
+}
+
+int dos_host_down(const float* x, void* out, int ot, int64_t n, int nthreads) {
+  const dos_hk_table& t = hk();
+  parallel_chunks(n, nthreads, [&](int64_t lo, int64_t hi) { t.down(x, out, ot, lo, hi); });
+  return DOS_OK;
+}
+
+extern "C" int dos_adam_step_host(float* p, float* m, float* v, const void* g, int g_dtype, void* p_lowp,
+                                  int lowp_dtype, int64_t n, const dos_adam_scalars* s, int nthreads) {
+  if (!s) return dos_set_error(DOS_EINVAL, "scalars must not be NULL");
+  if (n < 0) return dos_set_error(DOS_EINVAL, "n must be >= 0");
+  if (g_dtype != DOS_F32 && g_dtype != DOS_F16 && g_dtype != DOS_BF16)
+    return dos_set_error(DOS_ETYPE, "grad dtype %d unsupported", g_dtype);
+  if (lowp_dtype != DOS_NONE && lowp_dtype != DOS_F16 && lowp_dtype != DOS_BF16)
+    return dos_set_error(DOS_ETYPE, "working-copy dtype %d unsupported", lowp_dtype);
+  if (n == 0) return DOS_OK;
+  if (!p || !m || !v || !g || (lowp_dtype != DOS_NONE && !p_lowp)) return dos_set_error(DOS_EINVAL, "NULL buffer");
+  return dos_host_adam(p, m, v, g, g_dtype, p_lowp, lowp_dtype, n, dos_make_kscal(s), nthreads);
+}
+
+extern "C" int dos_downscale_host(const float* x, void* out, int out_dtype, int64_t n, int nthreads) {
+  if (n < 0) return dos_set_error(DOS_EINVAL, "n must be >= 0");
+  if (out_dtype != DOS_F16 && out_dtype != DOS_BF16)
+    return dos_set_error(DOS_ETYPE, "downscale target dtype %d unsupported", out_dtype);
+  if (n == 0) return DOS_OK;
+  if (!x || !out) return dos_set_error(DOS_EINVAL, "NULL buffer");
+  return dos_host_down(x, out, out_dtype, n, nthreads);
+}
+
+extern "C" int dos_upscale_host(const void* x, int in_dtype, float* out, int64_t n, int nthreads) {
+  if (n < 0) return dos_set_error(DOS_EINVAL, "n must be >= 0");
+  if (in_dtype != DOS_F16 && in_dtype != DOS_BF16)
+    return dos_set_error(DOS_ETYPE, "upscale source dtype %d unsupported", in_dtype);
+  if (n == 0) return DOS_OK;
+  if (!x || !out) return dos_set_error(DOS_EINVAL, "NULL buffer");
+  const dos_hk_table& t = hk();
+  parallel_chunks(n, nthreads, [&](int64_t lo, int64_t hi) { t.up(x, in_dtype, out, lo, hi); });
+  return DOS_OK;
+}
+
+// ---------------------------------------------------------------- pool
+// mmap -> MADV_HUGEPAGE -> optional mbind -> parallel first touch by the
+// team -> cudaHostRegister.  Registering pre-faulted 2 MB pages is far
+// cheaper than cudaHostAlloc's page-by-page pinning of a fresh range.
+namespace {
+struct Region {
+  size_t bytes;
+  bool registered;
+};
+std::mutex g_pool_mu;
+std::unordered_map<void*, Region> g_regions;
+
+long sys_mbind(void* addr, unsigned long len, int mode, const unsigned long* nodemask, unsigned long maxnode,
+               unsigned flags) {
+#ifdef SYS_mbind
+  return syscall(SYS_mbind, addr, len, mode, nodemask, maxnode, flags);
+#else
+  errno = ENOSYS;
+  return -1;
+#endif
+}
+}  // namespace
+
+extern "C" int dos_host_alloc(size_t bytes, int numa_node, int register_cuda, void** out) {
+  if (!out) return dos_set_error(DOS_EINVAL, "out must not be NULL");
+  *out = nullptr;
+  if (bytes == 0) bytes = 1;
+  const size_t huge = size_t(2) << 20;
+  const size_t len = (bytes + huge - 1) & ~(huge - 1);
+  void* ptr = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (ptr == MAP_FAILED) return dos_set_error(DOS_ESYS, "mmap(%zu) failed: %s", len, strerror(errno));
+  madvise(ptr, len, MADV_HUGEPAGE);
+  if (numa_node >= 0 && numa_node < 64) {
+    unsigned long mask = 1ul << numa_node;
+    if (sys_mbind(ptr, len, 2 /* MPOL_BIND */, &mask, 64, 0) != 0) {
+      // not fatal: single-node hosts and containers without CAP_SYS_NICE
+    }
+  }
+  // first touch in parallel, one 2 MB page at a time
+  char* base = static_cast<char*>(ptr);
+  const int64_t pages = (int64_t)(len / huge);
+  parallel_chunks(pages, 0, [&](int64_t lo, int64_t hi) {
+    for (int64_t i = lo; i < hi; ++i) memset(base + i * huge, 0, huge);
+  });
+  bool registered = false;
+  if (register_cuda) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0) {
+      const cudaError_t e = cudaHostRegister(ptr, len, cudaHostRegisterDefault);
+      if (e != cudaSuccess) {
+        munmap(ptr, len);
+        return dos_set_error(DOS_ECUDA, "cudaHostRegister(%zu) failed: %s", len, cudaGetErrorString(e));
+      }
+      registered = true;
+    } else {
+      cudaGetLastError();  // clear the no-device error; plain memory is still usable
+    }
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_regions[ptr] = Region{len, registered};
+  }
+  *out = ptr;
+  return DOS_OK;
+}
+
+extern "C" int dos_host_free(void* ptr) {
+  if (!ptr) return DOS_OK;
+  Region r;
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    auto it = g_regions.find(ptr);
+    if (it == g_regions.end()) return dos_set_error(DOS_EINVAL, "pointer %p was not allocated by dos_host_alloc", ptr);
+    r = it->second;
+    g_regions.erase(it);
+  }
+  if (r.registered) cudaHostUnregister(ptr);
+  munmap(ptr, r.bytes);
+  return DOS_OK;
+}

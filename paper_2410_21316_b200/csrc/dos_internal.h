@@ -1,0 +1,37 @@
+// dos_internal.h — declarations shared by the libdos translation units.
+#pragma once
+#include <stdint.h>
+
+#include "../../include/dos.h"
+#include "dos_numerics.h"
+
+#ifdef __CUDACC__
+#include <cuda_runtime.h>
+#else
+#include <cuda_runtime_api.h>
+#endif
+
+// Records a thread-local message (printf format) and returns `code`.
+int dos_set_error(int code, const char* fmt, ...);
+
+// Per-launch scalars from the C-ABI struct (fp32 arithmetic on the host).
+dos_kscal dos_make_kscal(const dos_adam_scalars* s);
+
+// K1 launch without argument validation (used by the engine).
+int dos_adam_launch(float* p, float* m, float* v, const void* g, int gt, void* lp, int lt, int64_t n,
+                    const dos_kscal& s, cudaStream_t st);
+
+// Host kernels (dos_host.cpp); the calling thread joins the team.
+int dos_host_adam(float* p, float* m, float* v, const void* g, int gt, void* lp, int lt, int64_t n,
+                  const dos_kscal& s, int nthreads);
+int dos_host_down(const float* x, void* out, int ot, int64_t n, int nthreads);
+
+// One ISA variant of the host loops (dos_host_isa.cpp, built per ISA).
+struct dos_hk_table {
+  void (*adam)(float*, float*, float*, const void*, int, void*, int, int64_t, int64_t, const dos_kscal&);
+  void (*down)(const float*, void*, int, int64_t, int64_t);
+  void (*up)(const void*, int, float*, int64_t, int64_t);
+};
+extern const dos_hk_table dos_hk_avx512;
+extern const dos_hk_table dos_hk_avx2;
+extern const dos_hk_table dos_hk_generic;

@@ -1,0 +1,337 @@
+"""B200 residency of a shard and the ``B200Target`` plugin.
+
+Memory layout of one rank on the B200 (HBM) and its host (pinned pool):
+
+  host (pinned, registered)          HBM
+  -------------------------          ---
+  params32/momentum32/variance32     grads        lowp[P]   (resident: backward/RS writes it)
+    fp32[P] — home tier of every     model16      lowp[P]   (authoritative working copy)
+    dynamic and CPU subgroup         static p/m/v fp32, compact, for static residents
+  grads16   lowp[P] — host image     slots[num_slots] x {m, v, p} fp32[SG_max]
+    used by CPU subgroups              (the in-flight windows; engine-owned)
+  model16   lowp[P] — staging for
+    CPU-downscaled params (H2D_PARAMS16 source) and the lazy host image
+
+``B200Target`` is the third implementation of the reference's UpdateTarget
+protocol (pkg/src/optistate/scheduler.py:388-399), after SimTarget and
+ExecutorTarget: durations/bytes come from the profile (so ``run_update``'s
+virtual timeline is the prediction and equals ``simulate_update_phase``),
+and ``apply`` hands each action to the native engine (dos_exec_submit),
+which enqueues it on the B200's copy/compute streams or the host lane and
+returns at once.  ``finish`` waits for the phase and returns the *measured*
+timeline.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from typing import Sequence
+
+import numpy as np
+
+from . import _native as N
+from .plan import KIND_CODE, LANE_CODE, ActionKind, ScheduledAction, UpdatePlan
+from .state import SUBGROUP_STATE_BYTES_PER_PARAM, ShardedOptimizer, SystemProfile, bias_corrections
+from .timing import SimTarget
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+class DeviceResidency:
+    """What of one ShardedOptimizer lives in HBM, and host/device coherence."""
+
+    def __init__(self, opt: ShardedOptimizer, device=None) -> None:
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise RuntimeError("no CUDA device visible: the B200 update phase needs a GPU (no CPU fallback)")
+        N.lib()  # fail loudly now if the native library is missing
+        self.opt = opt
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        self.tdtype = torch.float16 if opt.lowp == "fp16" else torch.bfloat16
+        P = opt.total_params
+        nsg = len(opt.subgroups)
+        with torch.cuda.device(self.device):
+            self.grads = torch.empty(P, dtype=self.tdtype, device=self.device)
+            self.model16 = torch.empty(P, dtype=self.tdtype, device=self.device)
+        self.sg_start = np.array([g.start for g in opt.subgroups], dtype=np.int64)
+        self.sg_size = np.array([g.size for g in opt.subgroups], dtype=np.int64)
+        self.static_set: frozenset[int] = frozenset()
+        self.static_off = np.full(nsg, -1, dtype=np.int64)
+        self.static_p = self.static_m = self.static_v = None
+        self.host_stale: set[str] = set()  # host images behind the device
+        self._engines: dict[tuple, "Engine"] = {}
+        self.push_host()
+
+    # ---- coherence
+    def _h2d(self, dst, src: np.ndarray) -> None:
+        torch = _torch()
+        dst.view(torch.int16 if dst.element_size() == 2 else torch.int32).copy_(
+            torch.from_numpy(src.view(np.int16 if src.itemsize == 2 else np.int32)), non_blocking=False)
+
+    def _d2h(self, dst: np.ndarray, src) -> None:
+        torch = _torch()
+        torch.from_numpy(dst.view(np.int16 if dst.itemsize == 2 else np.int32)).copy_(
+            src.view(torch.int16 if src.element_size() == 2 else torch.int32), non_blocking=False)
+
+    def push_host(self) -> None:
+        """Host arrays became authoritative (init, a host-side update): re-upload."""
+        opt = self.opt
+        self._h2d(self.grads, opt._g)
+        self._h2d(self.model16, opt._w)
+        for sg in self.static_set:
+            self._upload_static(sg)
+        self.host_stale.clear()
+
+    def sync_host(self, name: str) -> None:
+        if name not in self.host_stale:
+            return
+        self.host_stale.discard(name)
+        opt = self.opt
+        if name == "_w":
+            self._d2h(opt._w, self.model16)
+            return
+        src = {"_p": self.static_p, "_m": self.static_m, "_v": self.static_v}[name]
+        dst = getattr(opt, name)
+        for sg in self.static_set:
+            a, n, o = int(self.sg_start[sg]), int(self.sg_size[sg]), int(self.static_off[sg])
+            self._d2h(dst[a:a + n], src[o:o + n])
+
+    def sync_all_host(self) -> None:
+        for name in ("_w", "_p", "_m", "_v"):
+            self.sync_host(name)
+
+    def host_modified(self) -> None:
+        """Call after writing host arrays directly (e.g. a host-only update)."""
+        self.sync_all_host()
+        self.push_host()
+
+    def load_grads(self, grads) -> None:
+        """New step gradients: a CUDA tensor (flushed to the host image for
+        CPU subgroups) or a host array of the lowp kind (uploaded)."""
+        torch = _torch()
+        opt = self.opt
+        if isinstance(grads, torch.Tensor):
+            if grads.numel() != opt.total_params:
+                raise ValueError("grads must hold total_params elements")
+            src = grads.reshape(-1).to(device=self.device, dtype=self.tdtype)
+            self.grads.copy_(src)
+            self._d2h(opt._g, self.grads)
+            return
+        arr = np.asarray(grads)
+        if arr.dtype != opt._g.dtype or arr.shape != opt._g.shape:
+            raise TypeError(f"grads must be {opt._g.dtype}{opt._g.shape}")
+        opt._g[:] = arr
+        self._h2d(self.grads, opt._g)
+
+    def _upload_static(self, sg: int) -> None:
+        a, n, o = int(self.sg_start[sg]), int(self.sg_size[sg]), int(self.static_off[sg])
+        self._h2d(self.static_p[o:o + n], self.opt._p[a:a + n])
+        self._h2d(self.static_m[o:o + n], self.opt._m[a:a + n])
+        self._h2d(self.static_v[o:o + n], self.opt._v[a:a + n])
+
+    def set_static(self, static_set: frozenset[int]) -> None:
+        """Make exactly ``static_set`` HBM-resident (TwinFlow-style statics)."""
+        if static_set == self.static_set:
+            return
+        torch = _torch()
+        for name in ("_p", "_m", "_v"):
+            self.sync_host(name)
+        self.static_set = frozenset(static_set)
+        self.static_off[:] = -1
+        off = 0
+        for sg in sorted(self.static_set):
+            self.static_off[sg] = off
+            off += int(self.sg_size[sg])
+        if off:
+            with torch.cuda.device(self.device):
+                self.static_p = torch.empty(off, dtype=torch.float32, device=self.device)
+                self.static_m = torch.empty(off, dtype=torch.float32, device=self.device)
+                self.static_v = torch.empty(off, dtype=torch.float32, device=self.device)
+            for sg in self.static_set:
+                self._upload_static(sg)
+        else:
+            self.static_p = self.static_m = self.static_v = None
+
+    def after_phase(self) -> None:
+        self.host_stale.add("_w")
+        if self.static_set:
+            self.host_stale.update(("_p", "_m", "_v"))
+
+    # ---- engine cache
+    def engine(self, num_slots: int, slot_elems: int, host_threads: int = 0, fuse: bool = True) -> "Engine":
+        key = (num_slots, slot_elems, host_threads, fuse)
+        eng = self._engines.get(key)
+        if eng is None:
+            # one engine per residency: drop others (frees their HBM slots)
+            for e in self._engines.values():
+                e.close()
+            self._engines.clear()
+            eng = Engine(self.device.index, num_slots, slot_elems, host_threads, fuse)
+            self._engines[key] = eng
+        return eng
+
+    def state_desc(self) -> tuple[N.dos_state_desc, list]:
+        opt = self.opt
+        keep = [self.sg_start, self.sg_size, self.static_off]
+        p64 = C.POINTER(C.c_int64)
+        d = N.dos_state_desc(
+            num_subgroups=len(opt.subgroups),
+            sg_start=self.sg_start.ctypes.data_as(p64),
+            sg_size=self.sg_size.ctypes.data_as(p64),
+            static_offset=self.static_off.ctypes.data_as(p64),
+            lowp_dtype=opt.lowp_code,
+            host_p=N.ptr(opt._p), host_m=N.ptr(opt._m), host_v=N.ptr(opt._v),
+            host_g=N.ptr(opt._g), host_lowp=N.ptr(opt._w),
+            dev_g=self.grads.data_ptr(), dev_lowp=self.model16.data_ptr(),
+            dev_static_p=self.static_p.data_ptr() if self.static_p is not None else None,
+            dev_static_m=self.static_m.data_ptr() if self.static_m is not None else None,
+            dev_static_v=self.static_v.data_ptr() if self.static_v is not None else None,
+        )
+        return d, keep
+
+
+class Engine:
+    """Owner of one native engine (streams, HBM slots, host-lane worker)."""
+
+    def __init__(self, device: int, num_slots: int, slot_elems: int, host_threads: int = 0, fuse: bool = True):
+        cfg = N.dos_exec_config(device=device, num_slots=num_slots, slot_elems=slot_elems,
+                                host_threads=host_threads, fuse_downscale=1 if fuse else 0)
+        h = C.c_void_p()
+        N.check(N.lib().dos_exec_create(C.byref(cfg), C.byref(h)))
+        self.handle = h
+        self.num_slots = num_slots
+        self.slot_elems = slot_elems
+
+    def close(self) -> None:
+        if self.handle:
+            N.lib().dos_exec_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class _PlanDescs:
+    """The plan's actions as C structs, built once per plan object."""
+
+    def __init__(self, plan: UpdatePlan) -> None:
+        n = len(plan.actions)
+        self.descs = (N.dos_action_desc * n)()
+        self._keep = []
+        p32 = C.POINTER(C.c_int32)
+        for a in plan.actions:
+            d = self.descs[a.id]
+            d.id = a.id
+            d.kind = KIND_CODE[a.kind]
+            d.subgroup = a.subgroup
+            d.lane = LANE_CODE[a.lane]
+            d.is_static = 1 if (a.subgroup >= 0 and a.subgroup in plan.static_set) else 0
+            deps = np.array(a.deps, dtype=np.int32)
+            batch = np.array(a.batch, dtype=np.int32)
+            self._keep += [deps, batch]
+            d.num_deps = len(a.deps)
+            d.deps = deps.ctypes.data_as(p32)
+            d.batch_len = len(a.batch)
+            d.batch = batch.ctypes.data_as(p32)
+
+
+_DESC_CACHE: dict[int, tuple[UpdatePlan, _PlanDescs]] = {}
+
+
+def plan_descs(plan: UpdatePlan) -> _PlanDescs:
+    hit = _DESC_CACHE.get(id(plan))
+    if hit is not None and hit[0] is plan:
+        return hit[1]
+    if len(_DESC_CACHE) > 16:
+        _DESC_CACHE.clear()
+    pd = _PlanDescs(plan)
+    _DESC_CACHE[id(plan)] = (plan, pd)
+    return pd
+
+
+def slots_for(profile: SystemProfile, plan: UpdatePlan, sizes: Sequence[int]) -> tuple[int, int]:
+    """(physical windows, elements per window piece) for this plan."""
+    dyn = [sizes[i] for i in plan.dynamic_fast]
+    if not dyn:
+        return 1, 0
+    biggest = max(dyn)
+    cap = profile.fast_capacity_bytes
+    windows = 2 if cap is None else min(2, cap // (SUBGROUP_STATE_BYTES_PER_PARAM * biggest))
+    if windows < 1:
+        raise N.InfeasibleConfigError(
+            f"fast tier capacity {cap} B cannot hold one in-flight subgroup window of "
+            f"{SUBGROUP_STATE_BYTES_PER_PARAM * biggest} B")
+    return windows, biggest
+
+
+class B200Target(SimTarget):
+    """UpdateTarget that executes the plan on a B200 and its host.
+
+    Predicted durations/bytes are SimTarget's (from ``profile``); ``apply``
+    submits the action to the native engine without waiting.  Call
+    ``finish()`` after ``run_update`` to wait and get measured events.
+    """
+
+    def __init__(self, profile: SystemProfile, plan: UpdatePlan, optimizer: ShardedOptimizer, hyper,
+                 step: int, *, host_threads: int = 0, fuse_downscale: bool = True) -> None:
+        sizes = tuple(g.size for g in optimizer.subgroups)
+        super().__init__(profile, plan, sizes)
+        self.opt = optimizer
+        self.hyper = hyper
+        self.step = step
+        self.residency = optimizer.to_device()
+        self.residency.set_static(plan.static_set)
+        self.num_slots, slot_elems = slots_for(profile, plan, sizes)
+        self.engine = self.residency.engine(self.num_slots, slot_elems, host_threads, fuse_downscale)
+        self._descs = plan_descs(plan)
+        self._begun = False
+        self._submitted = 0
+
+    def _begin(self) -> None:
+        desc, keep = self.residency.state_desc()
+        self._keep = (desc, keep)
+        h = self.hyper
+        bc1, bc2 = bias_corrections(h.beta1, h.beta2, self.step)
+        sc = N.scalars(h.lr, h.beta1, h.beta2, h.eps, bc1, bc2, getattr(h, "weight_decay", 0.0))
+        self._sc = sc
+        N.check(N.lib().dos_exec_begin(self.engine.handle, C.byref(desc), C.byref(sc), len(self.plan.actions)))
+        self._begun = True
+
+    def apply(self, action, start_ns: int, end_ns: int) -> None:
+        if not self._begun:
+            self._begin()
+        rc = N.lib().dos_exec_submit(self.engine.handle, C.byref(self._descs.descs[action.id]))
+        self._submitted += 1
+        if rc != N.DOS_OK:
+            msg = N.lib().dos_last_error().decode(errors="replace")
+            self.finish(raise_errors=False)  # drain what was enqueued before failing
+            exc = {N.DOS_ESTATE: AssertionError, N.DOS_EINFEASIBLE: N.InfeasibleConfigError,
+                   N.DOS_EINVAL: ValueError, N.DOS_ETYPE: TypeError}.get(rc, RuntimeError)
+            raise exc(f"submit of action {action.id}: {msg}")
+
+    def finish(self, raise_errors: bool = True) -> tuple[ScheduledAction, ...]:
+        """Wait for the phase; measured events in emission order."""
+        if not self._begun:
+            return ()
+        n = self._submitted
+        s = np.zeros(max(n, 1), dtype=np.int64)
+        e = np.zeros(max(n, 1), dtype=np.int64)
+        p64 = C.POINTER(C.c_int64)
+        rc = N.lib().dos_exec_finish(self.engine.handle, s.ctypes.data_as(p64), e.ctypes.data_as(p64), n)
+        self._begun = False
+        if rc != N.DOS_OK:
+            if raise_errors:
+                N.check(rc)
+            return ()
+        acts = self.plan.actions
+        return tuple(ScheduledAction(action=acts[i], start_ns=int(s[i]), end_ns=int(e[i]),
+                                     bytes=self.bytes_of(acts[i])) for i in range(n))

@@ -1,0 +1,268 @@
+"""Step entry points of the update phase (reference: pkg/src/optistate/executor.py).
+
+* ``execute_plan`` runs one optimizer step of a plan on the B200 and its host
+  (``B200Target``): fast subgroups stream through HBM windows and K1, host
+  subgroups run H1 on the host team, the half-precision working copy ends in
+  HBM.  It returns the *predicted* timeline (identical to
+  ``simulate_update_phase``, as the reference guarantees,
+  pkg/tests/test_executor.py:79-86) and the *measured* one.
+* ``sequential_oracle`` / ``adam_step_subgroup`` are the reference's plain
+  in-order host update (executor.py:77-117), executed by H1.
+* ``flush_gradients`` materialises fp32 grads on the host (executor.py:317-349).
+"""
+
+from __future__ import annotations
+
+import enum
+import math
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .device import B200Target
+from .engine import run_update, validate_schedule
+from .plan import UpdatePlan
+from .state import GRADS16_BYTES_PER_PARAM, ShardedOptimizer, SystemProfile, bias_corrections, lowp_downscale
+from .timing import GradFlushStrategy, Timeline, build_timeline, grad_flush_throughput
+
+# Cross-clock slack when auditing measured timelines: host-lane events are
+# stamped with the host clock aligned to the phase's t0 CUDA event, device
+# events with the GPU clock.
+MEASURED_CLOCK_SLACK_NS = 200_000
+
+
+@dataclass(frozen=True)
+class AdamHyper:
+    """Adam hyperparameters (executor.py:45-56) plus optional decoupled
+    weight decay (AdamW; no reference pin)."""
+
+    lr: float = 1e-3
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    weight_decay: float = 0.0
+
+    def __post_init__(self) -> None:
+        if not (0.0 <= self.beta1 < 1.0 and 0.0 <= self.beta2 < 1.0):
+            raise ValueError("betas must be in [0, 1)")
+        if self.lr <= 0 or self.eps <= 0:
+            raise ValueError("lr and eps must be positive")
+        if self.weight_decay < 0:
+            raise ValueError("weight_decay must be >= 0")
+
+    def scalars(self, step: int) -> N.dos_adam_scalars:
+        bc1, bc2 = bias_corrections(self.beta1, self.beta2, step)
+        return N.scalars(self.lr, self.beta1, self.beta2, self.eps, bc1, bc2, self.weight_decay)
+
+
+class ExecMode(str, enum.Enum):
+    VIRTUAL = "virtual"
+    THROTTLED = "throttled"
+
+
+def _host_update(opt: ShardedOptimizer, sg_index: int, hyper: AdamHyper, step: int, refresh_lowp: bool) -> None:
+    sg = opt.subgroups[sg_index]
+    a, n = sg.start, sg.size
+    p, m, v, g, w = opt._p, opt._m, opt._v, opt._g, opt._w
+    item16 = g.itemsize
+    lp = N.ptr(w) + item16 * a if refresh_lowp else None
+    sc = hyper.scalars(step)
+    N.check(N.lib().dos_adam_step_host(N.ptr(p) + 4 * a, N.ptr(m) + 4 * a, N.ptr(v) + 4 * a, N.ptr(g) + item16 * a,
+                                       opt.lowp_code, lp, opt.lowp_code if refresh_lowp else N.DOS_NONE, n, sc, 0))
+
+
+def _host_authoritative(opt: ShardedOptimizer):
+    res = opt.residency
+    if res is not None:
+        res.sync_all_host()
+    return res
+
+
+def adam_step_subgroup(optimizer: ShardedOptimizer, subgroup: int, hyper: AdamHyper, step: int | None = None) -> None:
+    """Fused Adam on one subgroup's master state, in place, on the host.
+
+    Grads are widened from the half-precision copy inside H1.  ``model16`` is
+    left stale (the refresh is a separate action); the caller owns the step
+    bump (executor.py:77-100).
+    """
+    res = _host_authoritative(optimizer)
+    _host_update(optimizer, subgroup, hyper, optimizer.step + 1 if step is None else step, refresh_lowp=False)
+    if res is not None:
+        res.push_host()
+
+
+def sequential_oracle(optimizer: ShardedOptimizer, hyper: AdamHyper) -> ShardedOptimizer:
+    """Every subgroup in order on the host: Adam, then the working-copy
+    refresh (fused into the same H1 pass); bumps ``step`` (executor.py:103-117)."""
+    res = _host_authoritative(optimizer)
+    step = optimizer.step + 1
+    for sg in optimizer.subgroups:
+        _host_update(optimizer, sg.index, hyper, step, refresh_lowp=True)
+    optimizer.step = step
+    if res is not None:
+        res.push_host()
+    return optimizer
+
+
+class EmulatedDevice:
+    """Structural staging ledger (executor.py:120-171): double stages,
+    incomplete triplets and undrained windows are schedule bugs.  The native
+    engine enforces the same rules on the real HBM slots; this class keeps
+    the reference's pure-Python form for planners and tests."""
+
+    PIECES = ("m", "v", "p")
+
+    def __init__(self) -> None:
+        self.staging: dict[int, dict[str, np.ndarray]] = {}
+        self.model16_valid: set[int] = set()
+
+    def stage(self, subgroup: int, piece: str, data: np.ndarray) -> None:
+        slot = self.staging.setdefault(subgroup, {})
+        if piece in slot:
+            raise AssertionError(f"subgroup {subgroup} piece {piece!r} staged twice")
+        slot[piece] = data
+
+    def staged(self, subgroup: int, piece: str) -> np.ndarray:
+        slot = self.staging.get(subgroup, {})
+        if piece not in slot:
+            raise AssertionError(f"subgroup {subgroup} piece {piece!r} not resident on device")
+        return slot[piece]
+
+    def require_triplet(self, subgroup: int) -> dict[str, np.ndarray]:
+        slot = self.staging.get(subgroup, {})
+        missing = [p for p in self.PIECES if p not in slot]
+        if missing:
+            raise AssertionError(f"fast update of subgroup {subgroup} with missing pieces {missing}")
+        return slot
+
+    def unstage(self, subgroup: int, piece: str) -> np.ndarray:
+        data = self.staged(subgroup, piece)
+        slot = self.staging[subgroup]
+        del slot[piece]
+        if not slot:
+            del self.staging[subgroup]
+        return data
+
+    def assert_drained(self) -> None:
+        if self.staging:
+            raise AssertionError(f"staging store not drained: subgroups {sorted(self.staging)}")
+
+
+@dataclass(frozen=True)
+class ExecutionResult:
+    optimizer: ShardedOptimizer
+    timeline: Timeline  # predicted (== simulate_update_phase of the same plan/profile/sizes)
+    step: int
+    mode: ExecMode
+    measured: Timeline | None = None  # wall-clock timeline of the B200 run
+
+
+def execute_plan(
+    optimizer: ShardedOptimizer,
+    plan: UpdatePlan,
+    profile: SystemProfile,
+    hyper: AdamHyper,
+    mode: ExecMode = ExecMode.VIRTUAL,
+    throttle_scale: float = 1e-3,
+    *,
+    host_threads: int = 0,
+    check_coherence: bool = False,
+    validate_measured: bool = True,
+) -> ExecutionResult:
+    """Run one optimizer step of ``plan`` on the B200; mutates ``optimizer``.
+
+    Same contract as executor.py:246-293: raises ValueError on a plan/shard
+    size mismatch, audits the schedule, requires the staging windows to
+    drain, bumps ``step``.  ``check_coherence`` re-derives the working copy
+    from the fp32 params and compares bitwise (the reference always does;
+    here it is opt-in because it is a full extra pass).
+    """
+    if plan.num_subgroups != len(optimizer.subgroups):
+        raise ValueError(f"plan covers {plan.num_subgroups} subgroups, optimizer has {len(optimizer.subgroups)}")
+    if mode is ExecMode.THROTTLED and throttle_scale <= 0:
+        raise ValueError("throttle_scale must be positive")
+    step = optimizer.step + 1
+    target = B200Target(profile, plan, optimizer, hyper, step, host_threads=host_threads)
+    try:
+        events = run_update(plan, target)
+    except BaseException:
+        target.finish(raise_errors=False)
+        raise
+    measured_events = target.finish()
+    validate_schedule(plan, events, target)
+    target.residency.after_phase()
+    sizes = target.sizes
+    measured = build_timeline(plan, measured_events, sizes) if measured_events else None
+    if validate_measured and measured_events:
+        validate_schedule(plan, measured_events, target, check_streams=False, max_windows=target.num_slots,
+                          tolerance_ns=MEASURED_CLOCK_SLACK_NS)
+    optimizer.step = step
+    if check_coherence:
+        w = optimizer.model16
+        want = lowp_downscale(optimizer.params32, optimizer.lowp)
+        for sg in optimizer.subgroups:
+            if want[sg.slice].tobytes() != w[sg.slice].tobytes():
+                raise AssertionError(f"model16 of subgroup {sg.index} incoherent with params32")
+    timeline = build_timeline(plan, events, sizes)
+    if mode is ExecMode.THROTTLED:
+        _pace_replay(timeline, throttle_scale)
+    return ExecutionResult(optimizer=optimizer, timeline=timeline, step=step, mode=mode, measured=measured)
+
+
+def _pace_replay(timeline: Timeline, scale: float) -> None:
+    if scale <= 0:
+        raise ValueError("throttle_scale must be positive")
+    t0 = time.perf_counter()
+    for ev in sorted(timeline.events, key=lambda e: e.start_ns):
+        wait = t0 + ev.start_ns * 1e-9 * scale - time.perf_counter()
+        if wait > 0:
+            time.sleep(wait)
+
+
+@dataclass(frozen=True)
+class GradFlushRecord:
+    strategy: GradFlushStrategy
+    payload_bytes: int
+    chunk_bytes: int
+    throughput_bytes_per_s: float
+    cost_ns: int
+
+
+def flush_gradients(optimizer: ShardedOptimizer, profile: SystemProfile, strategy: GradFlushStrategy,
+                    chunk_bytes: int = 1 << 22) -> tuple[np.ndarray, GradFlushRecord]:
+    """fp32 host gradients plus the modelled cost of the strategy.
+
+    Numerically the exact widening of the half-precision grads, identical for
+    every strategy and chunk size (executor.py:317-349).  With a B200
+    residency the GPU_UPSCALE_FP32 leg runs on the device (dos_upscale_cuda)
+    followed by a pinned D2H; otherwise H1 widens the host image.
+    """
+    if chunk_bytes < 2:
+        raise ValueError("chunk_bytes must hold at least one fp16 element")
+    P = optimizer.total_params
+    out = np.empty(P, dtype=np.float32)
+    elems = chunk_bytes // 2
+    res = optimizer.residency
+    g = optimizer.grads16
+    if res is not None and strategy is GradFlushStrategy.GPU_UPSCALE_FP32:
+        import torch
+
+        buf = torch.empty(min(elems, P), dtype=torch.float32, device=res.device)
+        host = torch.from_numpy(out)
+        stream = torch.cuda.current_stream(res.device).cuda_stream
+        for lo in range(0, P, elems):
+            hi = min(lo + elems, P)
+            N.check(N.lib().dos_upscale_cuda(res.grads.data_ptr() + 2 * lo, optimizer.lowp_code, buf.data_ptr(),
+                                             hi - lo, stream))
+            host[lo:hi].copy_(buf[:hi - lo])
+    else:
+        for lo in range(0, P, elems):
+            hi = min(lo + elems, P)
+            N.check(N.lib().dos_upscale_host(N.ptr(g) + 2 * lo, optimizer.lowp_code, N.ptr(out) + 4 * lo, hi - lo, 0))
+    payload = GRADS16_BYTES_PER_PARAM * P
+    rate = grad_flush_throughput(strategy, profile, payload)
+    rec = GradFlushRecord(strategy=strategy, payload_bytes=payload, chunk_bytes=chunk_bytes,
+                          throughput_bytes_per_s=rate, cost_ns=math.ceil(payload / rate * 1e9))
+    return out, rec

@@ -1,0 +1,148 @@
+"""execute_plan on the B200: every plan shape reproduces the reference's
+sequential update bit for bit (fp16 kind: against the reference's own
+digests; bf16 kind: against the oracle), with the measured timeline audited."""
+from __future__ import annotations
+
+import dataclasses
+import hashlib
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import optistate_oracle as O
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+import paper_2410_21316_b200 as D  # noqa: E402
+from paper_2410_21316_b200 import ALL_CPU, Placement  # noqa: E402
+
+STATES = json.loads((Path(__file__).resolve().parent / "golden" / "states.json").read_text())
+HYPER = D.AdamHyper()
+
+
+def digest(opt) -> str:
+    h = hashlib.sha256()
+    for a in (opt.params32, opt.momentum32, opt.variance32, opt.model16, opt.grads16):
+        h.update(a.tobytes())
+    return h.hexdigest()
+
+
+def oracle_digest(total, sg, seed, lowp="fp16", steps=1, **hyper):
+    st = O.initialize(total, sg, seed, lowp)
+    for _ in range(steps):
+        O.sequential_oracle(st, **hyper)
+    return O.state_digest(st)
+
+
+@pytest.mark.parametrize("stride", [1, 2, 3, ALL_CPU])
+@pytest.mark.parametrize("ratio", [0.0, 0.25])
+@pytest.mark.parametrize("placement", list(Placement))
+def test_any_plan_matches_oracle(h100, stride, ratio, placement):
+    opt = D.ShardedOptimizer.initialize(10 * 1024, 1024, seed=11)
+    plan = D.build_plan(10, stride, static_ratio=ratio, placement=placement)
+    res = D.execute_plan(opt, plan, h100, HYPER, check_coherence=True)
+    assert res.step == 1 and opt.step == 1
+    assert digest(opt) == STATES["oracle"]["10240|1024|11|1"]
+    assert res.measured is not None and len(res.measured.events) == len(plan.actions)
+
+
+def test_acceptance_instances_on_b200(h100):
+    """The reference's 236 schedule-independence instances (test_acceptance.py:121-175)."""
+    for inst in STATES["acceptance"]:
+        opt = D.ShardedOptimizer.initialize(inst["total"], inst["sg"], seed=inst["seed"])
+        plan = D.build_plan(len(opt.subgroups), inst["stride"], static_ratio=inst["ratio"],
+                            placement=Placement(inst["placement"]))
+        D.execute_plan(opt, plan, h100, D.AdamHyper(**inst["hyper"]))
+        assert digest(opt) == inst["digest"], inst
+    for stride in range(1, 7):
+        for ratio in (0.0, 0.25, 0.5):
+            for pl in Placement:
+                opt = D.ShardedOptimizer.initialize(12 * 257, 257, seed=4242)
+                D.execute_plan(opt, D.build_plan(12, stride, ratio, pl), h100, HYPER)
+                assert digest(opt) == STATES["fixed_4242"]
+
+
+def test_ragged_consecutive_and_replanned_steps(h100):
+    opt = D.ShardedOptimizer.initialize(5000, 1024, seed=5)
+    D.execute_plan(opt, D.build_plan(5, 2), h100, HYPER)
+    assert digest(opt) == oracle_digest(5000, 1024, 5)
+    opt = D.ShardedOptimizer.initialize(2048, 512, seed=2)
+    D.execute_plan(opt, D.build_plan(4, 2), h100, HYPER)
+    D.execute_plan(opt, D.build_plan(4, 3, 0.25), h100, HYPER)  # re-plan: subgroups change tier
+    assert opt.step == 2 and digest(opt) == STATES["oracle"]["2048|512|2|2"]
+
+
+def test_custom_hyper_and_bf16_kind(h100):
+    hyper = D.AdamHyper(lr=3e-4, beta1=0.8, beta2=0.95, eps=1e-6)
+    opt = D.ShardedOptimizer.initialize(1536, 256, seed=8)
+    D.execute_plan(opt, D.build_plan(6, 3, static_ratio=0.3, placement=Placement.STATIC_FIRST), h100, hyper)
+    assert digest(opt) == oracle_digest(1536, 256, 8, lr=3e-4, beta1=0.8, beta2=0.95, eps=1e-6)
+    for stride in (1, 2, 3, ALL_CPU):
+        opt = D.ShardedOptimizer.initialize(70_000, 7_000, seed=3, lowp="bf16")
+        D.execute_plan(opt, D.build_plan(10, stride, 0.2), h100, HYPER)
+        D.execute_plan(opt, D.build_plan(10, stride, 0.2), h100, HYPER)
+        assert digest(opt) == oracle_digest(70_000, 7_000, 3, "bf16", steps=2)
+
+
+def test_adamw_matches_oracle(h100):
+    hyper = D.AdamHyper(weight_decay=0.01)
+    opt = D.ShardedOptimizer.initialize(40_000, 4_000, seed=4, lowp="bf16")
+    D.execute_plan(opt, D.build_plan(10, 2, 0.2), h100, hyper)
+    assert digest(opt) == oracle_digest(40_000, 4_000, 4, "bf16", weight_decay=0.01)
+
+
+def test_predicted_timeline_equals_simulator_and_measured_validates(h100):
+    opt = D.ShardedOptimizer.initialize(8 * 256, 256, seed=4)
+    plan = D.build_plan(8, 2, static_ratio=0.25)
+    sim = D.simulate_update_phase(plan, h100, [g.size for g in opt.subgroups])
+    res = D.execute_plan(opt, plan, h100, HYPER)
+    assert res.timeline.events == sim.events and res.timeline.makespan_ns == sim.makespan_ns
+    m = res.measured
+    assert m.makespan_ns > 0 and m.span_ns >= m.makespan_ns
+    assert {e.action.id for e in m.events} == set(range(len(plan.actions)))
+
+
+def test_single_window_capacity(h100):
+    prof = dataclasses.replace(h100, fast_capacity_bytes=12 * 1000)
+    opt = D.ShardedOptimizer.initialize(8000, 1000, seed=9)
+    res = D.execute_plan(opt, D.build_plan(8, 1), prof, HYPER)
+    assert digest(opt) == oracle_digest(8000, 1000, 9)
+    with pytest.raises(D.InfeasibleConfigError):
+        D.execute_plan(D.ShardedOptimizer.initialize(8000, 1000, seed=9), D.build_plan(8, 1),
+                       dataclasses.replace(h100, fast_capacity_bytes=11_999), HYPER)
+    assert res.measured is not None
+
+
+def test_large_subgroups_sampled(h100):
+    """Four 25M-param subgroups, bf16, stride 2: property check at size."""
+    total, sg = 100_000_000, 25_000_000
+    opt = D.ShardedOptimizer.initialize(total, sg, seed=1, lowp="bf16")
+    want = O.initialize(total, sg, 1, "bf16")
+    D.execute_plan(opt, D.build_plan(4, 2), h100, HYPER)
+    O.sequential_oracle(want)
+    assert np.array_equal(opt.params32.view(np.uint32), want["p"].view(np.uint32))
+    assert np.array_equal(opt.variance32.view(np.uint32), want["v"].view(np.uint32))
+    assert np.array_equal(opt.model16, want["w"])
+
+
+def test_flush_gradients_device_path(h100):
+    opt = D.ShardedOptimizer.initialize(300_000, 70_000, seed=6, lowp="bf16")
+    opt.to_device()
+    out, rec = D.flush_gradients(opt, h100, D.GradFlushStrategy.GPU_UPSCALE_FP32, chunk_bytes=1 << 16)
+    assert out.tobytes() == O.f32_from_bf16(opt.grads16).tobytes()
+
+
+def test_load_grads_from_device_tensor(h100):
+    opt = D.ShardedOptimizer.initialize(20_000, 5_000, seed=2, lowp="bf16")
+    res = opt.to_device()
+    g = torch.randn(20_000, device="cuda").to(torch.bfloat16)
+    opt.load_grads(g)
+    assert np.array_equal(opt.grads16, g.view(torch.int16).cpu().numpy().view(np.uint16))
+    want = O.initialize(20_000, 5_000, 2, "bf16")
+    want["g"] = opt.grads16.copy()
+    D.execute_plan(opt, D.build_plan(4, 2), h100, HYPER)
+    O.sequential_oracle(want)
+    assert opt.params32.tobytes() == want["p"].tobytes() and res.model16.view(torch.int16).cpu().numpy().view(
+        np.uint16).tobytes() == want["w"].tobytes()

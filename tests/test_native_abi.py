@@ -1,0 +1,136 @@
+"""libdos.so: loads without a GPU, exports every include/dos.h symbol, maps
+errors to the reference's exception types, and H1 (host) is bit-exact."""
+from __future__ import annotations
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import optistate_oracle as O
+import paper_2410_21316_b200 as D
+from paper_2410_21316_b200 import _native as N
+
+HEADER = Path(__file__).resolve().parent.parent / "include" / "dos.h"
+
+
+def test_library_exports_every_declared_symbol():
+    lib = N.lib()
+    declared = set(re.findall(r"\b(dos_[a-z0-9_]+)\s*\(", HEADER.read_text()))
+    assert declared, "no declarations parsed"
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert declared == set(N.SIGNATURES), declared ^ set(N.SIGNATURES)
+    assert lib.dos_version() >= 1
+
+
+def test_error_codes_map_to_reference_exceptions():
+    lib = N.lib()
+    sc = N.scalars(1e-3, 0.9, 0.999, 1e-8, 0.1, 0.001)
+    x = np.zeros(4, np.float32)
+    with pytest.raises(TypeError):
+        N.check(lib.dos_adam_step_host(x.ctypes.data, x.ctypes.data, x.ctypes.data, x.ctypes.data, 7, None, -1, 4, sc, 0))
+    with pytest.raises(ValueError):
+        N.check(lib.dos_adam_step_host(x.ctypes.data, x.ctypes.data, x.ctypes.data, x.ctypes.data, 0, None, -1, -1, sc, 0))
+    with pytest.raises(ValueError):
+        N.check(lib.dos_host_free(12345))
+
+
+def _state(n, seed):
+    rng = np.random.default_rng(seed)
+    p = rng.normal(0, 0.02, n).astype(np.float32)
+    m = rng.normal(0, 1e-3, n).astype(np.float32)
+    v = (rng.random(n) * 1e-4).astype(np.float32)
+    g = rng.normal(0, 1.0, n).astype(np.float32)
+    return p, m, v, g
+
+
+@pytest.mark.parametrize("n", [0, 1, 7, 64, 1000, 65_537, 300_001])
+@pytest.mark.parametrize("step", [1, 7])
+def test_adam_step_arrays_host_bit_exact(n, step):
+    p, m, v, g = _state(n, n + step)
+    rp, rm, rv = p.copy(), m.copy(), v.copy()
+    D.adam_step_arrays(p, m, v, g, 1e-3, 0.9, 0.999, 1e-8, step)
+    if n:
+        O.adam_step(rp, rm, rv, g, 1e-3, 0.9, 0.999, 1e-8, step)
+    assert p.tobytes() == rp.tobytes() and m.tobytes() == rm.tobytes() and v.tobytes() == rv.tobytes()
+
+
+@pytest.mark.parametrize("lowp", ["fp16", "bf16"])
+@pytest.mark.parametrize("wd", [0.0, 0.01])
+def test_host_fused_lowp_grads_and_working_copy(lowp, wd):
+    n = 200_003
+    p, m, v, g32 = _state(n, 9)
+    g = O.lowp_from_f32(g32, lowp)
+    w = np.empty(n, dtype=np.uint16)
+    rp, rm, rv = p.copy(), m.copy(), v.copy()
+    sc = N.scalars(3e-4, 0.85, 0.99, 1e-7, *O.bias_corrections(0.85, 0.99, 4), weight_decay=wd)
+    N.check(N.lib().dos_adam_step_host(p.ctypes.data, m.ctypes.data, v.ctypes.data, g.ctypes.data,
+                                       N.LOWP_CODES[lowp], w.ctypes.data, N.LOWP_CODES[lowp], n, sc, 0))
+    O.adam_step(rp, rm, rv, O.f32_from_lowp(g, lowp), 3e-4, 0.85, 0.99, 1e-7, 4, weight_decay=wd)
+    assert p.tobytes() == rp.tobytes() and m.tobytes() == rm.tobytes() and v.tobytes() == rv.tobytes()
+    assert w.tobytes() == O.lowp_from_f32(rp, lowp).view(np.uint16).tobytes()
+
+
+def test_adam_step_arrays_validation():
+    p, m, v, g = _state(4, 0)
+    with pytest.raises(ValueError):
+        D.adam_step_arrays(p, m, v, g, 1e-3, 0.9, 0.999, 1e-8, 0)
+    with pytest.raises(TypeError):
+        D.adam_step_arrays(p.astype(np.float64), m, v, g, 1e-3, 0.9, 0.999, 1e-8, 1)
+    with pytest.raises(TypeError):
+        D.adam_step_arrays(p, m, v, g.astype(np.float16), 1e-3, 0.9, 0.999, 1e-8, 1)
+    with pytest.raises(ValueError):
+        D.adam_step_arrays(p, m, v, g[:2], 1e-3, 0.9, 0.999, 1e-8, 1)
+
+
+def test_backend_env_flag(tmp_path):
+    import os
+    import subprocess
+    import sys
+
+    root = str(Path(__file__).resolve().parent.parent)
+    ok = subprocess.run([sys.executable, "-c", "import paper_2410_21316_b200.kernels as k; assert k.active_backend()=='native'"],
+                        env=dict(os.environ, OPTISTATE_BACKEND="numpy", PYTHONPATH=root), capture_output=True, text=True)
+    assert ok.returncode == 0, ok.stderr
+    bad = subprocess.run([sys.executable, "-c", "import paper_2410_21316_b200.kernels"],
+                         env=dict(os.environ, OPTISTATE_BACKEND="cuda", PYTHONPATH=root), capture_output=True, text=True)
+    assert bad.returncode != 0 and "OPTISTATE_BACKEND" in bad.stderr
+
+
+def test_downscale_matches_golden_bits_including_nan_payloads():
+    d = np.load(Path(__file__).resolve().parent / "golden" / "fp16_vectors.npz")
+    got = D.downscale_rne(d["f32_bits"].view(np.float32)).view(np.uint16)
+    assert np.array_equal(got, d["f16_bits"])
+
+
+def test_fp16_roundtrip_exhaustive():
+    all16 = np.arange(2**16, dtype=np.uint16)
+    back = D.downscale_rne(D.upscale(all16.view(np.float16))).view(np.uint16)
+    assert np.array_equal(all16, back)
+    # widening equals numpy's, payloads included
+    assert D.upscale(all16.view(np.float16)).view(np.uint32).tobytes() == all16.view(np.float16).astype(np.float32).view(np.uint32).tobytes()
+
+
+def test_bf16_conversions_match_oracle():
+    rng = np.random.default_rng(5)
+    x = rng.integers(0, 2**32, 500_000, dtype=np.uint32).view(np.float32)
+    assert np.array_equal(D.downscale_bf16(x), O.bf16_from_f32(x))
+    b = np.arange(2**16, dtype=np.uint16)
+    assert D.upscale_bf16(b).view(np.uint32).tobytes() == O.f32_from_bf16(b).view(np.uint32).tobytes()
+
+
+def test_conversion_type_errors():
+    with pytest.raises(TypeError):
+        D.downscale_rne(np.zeros(3, dtype=np.float64))
+    with pytest.raises(TypeError):
+        D.upscale(np.zeros(3, dtype=np.float32))
+
+
+def test_pinned_pool_alloc_roundtrip():
+    buf = N.HostBuffer(3 << 20, register_cuda=False)
+    a = buf.array(np.float32, 1000)
+    a[:] = np.arange(1000, dtype=np.float32)
+    assert a.sum() == np.arange(1000, dtype=np.float32).sum()
+    assert a.ctypes.data % 4096 == 0

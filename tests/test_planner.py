@@ -1,0 +1,302 @@
+"""Planner, engine, perf model and timing model: bit-identical to the
+reference (goldens from tests/golden/make_goldens.py) plus the reference's
+behavioural checks (pkg/tests/test_scheduler.py, test_perfmodel.py,
+test_sim.py) restated."""
+from __future__ import annotations
+
+import copy
+import dataclasses
+import hashlib
+import json
+import math
+import pickle
+import warnings
+from fractions import Fraction
+from pathlib import Path
+
+import pytest
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+import paper_2410_21316_b200 as D
+from paper_2410_21316_b200 import ALL_CPU, ActionKind, Device, Lane, Placement, build_plan
+
+G = Path(__file__).resolve().parent / "golden"
+PLANS = json.loads((G / "plans.json").read_text())
+SIM = json.loads((G / "sim.json").read_text())
+PERF = json.loads((G / "perfmodel.json").read_text())
+
+
+def plan_canon(plan) -> str:
+    parts = [
+        f"n={plan.num_subgroups}",
+        "static=" + ",".join(map(str, sorted(plan.static_set))),
+        "dev=" + "".join("F" if d.value == "fast" else "C" for d in plan.devices),
+        "dyn=" + ",".join(map(str, plan.dynamic_fast)),
+        f"blocking={int(plan.blocking)}",
+    ]
+    for a in plan.actions:
+        parts.append(f"{a.id}:{a.kind.value}:{a.subgroup}:{a.lane.value}:{a.stream.value if a.stream else '-'}:"
+                     f"{','.join(map(str, a.batch))}:{','.join(map(str, a.deps))}")
+    return "\n".join(parts)
+
+
+def events_canon(events) -> str:
+    return "\n".join(f"{e.action.id}:{e.start_ns}:{e.end_ns}:{e.bytes}" for e in events)
+
+
+def sha(s: str) -> str:
+    return hashlib.sha256(s.encode()).hexdigest()
+
+
+def _stride(s: str):
+    return ALL_CPU if s == "all_cpu" else int(s)
+
+
+# ------------------------------------------------------------------ plans
+
+
+def test_every_golden_plan_is_bit_identical():
+    bad = []
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        for key, digest in PLANS["digests"].items():
+            n, s, r, pl = key.split("|")
+            plan = build_plan(int(n), _stride(s), float(r), Placement(pl))
+            if sha(plan_canon(plan)) != digest:
+                bad.append(key)
+    assert not bad, bad[:10]
+    assert len(PLANS["digests"]) > 4000
+
+
+@pytest.mark.parametrize("key", sorted(PLANS["full"]))
+def test_full_plan_listings(key):
+    n, s, r, pl = key.split("|")
+    assert plan_canon(build_plan(int(n), _stride(s), float(r), Placement(pl))) == PLANS["full"][key]
+
+
+def test_assignment_goldens():
+    plan = build_plan(8, 3, static_ratio=0.25, placement=Placement.STATIC_LAST)
+    assert {i for i, d in enumerate(plan.devices) if d is Device.FAST} == {2, 5, 6, 7}
+    assert all(d is Device.FAST for d in build_plan(4, 1).devices)
+    plan = build_plan(3, ALL_CPU, static_ratio=0.2, placement=Placement.STATIC_FIRST)
+    assert plan.static_set == frozenset() and all(d is Device.CPU for d in plan.devices)
+    assert build_plan(8, 2).dynamic_fast == (1, 3, 5, 7)
+    assert build_plan(12, 3).dynamic_fast == (2, 5, 8, 11)
+    assert build_plan(8, 2, 0.25, Placement.STATIC_FIRST).dynamic_fast == (3, 5, 7)
+    assert build_plan(8, 2, 0.25, Placement.STATIC_LAST).static_set == frozenset({6, 7})
+    assert [build_plan(10, 2, static_ratio=r).static_count for r in (0.3, 0.25)] == [3, 2]
+    assert build_plan(7, 2, static_ratio=0.1).static_count == 0
+
+
+def test_prev_next_on_gpu():
+    plan = build_plan(12, 3)
+    assert (D.prev_on_gpu(plan, 2), D.prev_on_gpu(plan, 5), D.prev_on_gpu(plan, 6)) == (None, 2, 5)
+    assert (D.next_on_gpu(plan, 6), D.next_on_gpu(plan, 8), D.next_on_gpu(plan, 11)) == (8, 11, None)
+
+
+def test_build_plan_validation_and_warning():
+    for args in ((-1, 2), (4, 0), (4, 2.5)):
+        with pytest.raises(ValueError):
+            build_plan(*args)
+    for r in (1.5, -0.1):
+        with pytest.raises(ValueError):
+            build_plan(4, 2, static_ratio=r)
+    with pytest.warns(UserWarning, match="all-static"):
+        plan = build_plan(4, 2, static_ratio=1.0)
+    assert plan.static_count == 4 and plan.dynamic_fast == ()
+
+
+def test_downscale_batches_and_cycle_start_pumping():
+    plan = build_plan(10, 3)
+    assert [a.batch for a in plan.actions if a.kind is ActionKind.CPU_DOWNSCALE] == [(0, 1), (3, 4), (6, 7), (9,)]
+    seq = [(a.kind, a.subgroup) for a in plan.actions]
+    assert (seq.index((ActionKind.GPU_UPDATE, 2)) < seq.index((ActionKind.FLUSH_OUT_MODEL16, 2))
+            < seq.index((ActionKind.PREFETCH_M, 5)) < seq.index((ActionKind.CPU_UPDATE, 3)))
+
+
+# ------------------------------------------------------------------ engine
+
+
+class UnitTarget:
+    def __init__(self, capacity=None, window=12):
+        self.fast_capacity_bytes = capacity
+        self._w = window
+        self.applied = []
+
+    def duration_ns(self, action):
+        return 10
+
+    def bytes_of(self, action):
+        return 0
+
+    def window_bytes(self, subgroup):
+        return self._w
+
+    def apply(self, action, start_ns, end_ns):
+        self.applied.append(action.id)
+
+
+def test_engine_grid_validates_and_applies_in_emission_order():
+    for stride in (1, 2, 3, ALL_CPU):
+        for ratio in (0.0, 0.25):
+            for pl in Placement:
+                for n in (0, 1, 2, 5, 8, 12):
+                    plan = build_plan(n, stride, ratio, pl)
+                    t = UnitTarget()
+                    sched = D.run_update(plan, t)
+                    D.validate_schedule(plan, sched, t)
+                    assert t.applied == list(range(len(plan.actions)))
+
+
+def test_blocking_plan_is_serial():
+    plan = build_plan(4, ALL_CPU)
+    sched = D.run_update(plan, UnitTarget())
+    for prev, ev in zip(sched, sched[1:]):
+        assert ev.start_ns == prev.end_ns and prev.action.id in ev.action.deps
+
+
+def test_capacity_gate():
+    plan = build_plan(8, 2)
+    tight, roomy = UnitTarget(capacity=12), UnitTarget(capacity=24)
+    s1, s2 = D.run_update(plan, tight), D.run_update(plan, roomy)
+    D.validate_schedule(plan, s1, tight)
+    D.validate_schedule(plan, s2, roomy)
+    assert max(e.end_ns for e in s1) > max(e.end_ns for e in s2)
+    with pytest.raises(D.InfeasibleConfigError):
+        D.run_update(build_plan(4, 2), UnitTarget(capacity=11))
+
+
+def test_validator_catches_tampering():
+    plan = build_plan(6, 2)
+    t = UnitTarget()
+    sched = list(D.run_update(plan, t))
+    cpu = [i for i, e in enumerate(sched) if e.action.lane is Lane.CPU_COMPUTE]
+    v = sched[cpu[1]]
+    sched[cpu[1]] = dataclasses.replace(v, start_ns=0, end_ns=v.duration_ns)
+    with pytest.raises(AssertionError):
+        D.validate_schedule(plan, sched, t)
+
+
+# ------------------------------------------------------------------ perf model
+
+
+def test_perfmodel_goldens():
+    for name in ("v100-node", "h100-node"):
+        prof = D.get_profile(name)
+        r = D.optimal_stride(prof)
+        assert r.k_real == PERF[name]["k_real"]
+        assert str(r.k) == PERF[name]["k"]
+        for key, want in PERF[name]["est"].items():
+            k, st_ = key.split("|")
+            assert D.estimate_update_time(prof, 40, 10**8, ALL_CPU if k == "all" else int(k), int(st_)) == want
+    for item in PERF["random"]:
+        prof = D.SystemProfile(**item["profile"])
+        r = D.optimal_stride(prof)
+        assert (r.k_real if math.isfinite(r.k_real) else "inf") == item["k_real"]
+        assert ("all_cpu" if r.k is ALL_CPU else str(r.k)) == item["k"]
+
+
+def test_k_real_against_rational_oracle(v100, h100):
+    for prof, frozen in ((v100, 2.294505494505494), (h100, 1.4898994734322641)):
+        b = Fraction(prof.channel_params_per_s)
+        num = 3 / b + 1 / Fraction(prof.fast_update_params_per_s)
+        den = 1 / Fraction(prof.cpu_update_params_per_s) + 1 / Fraction(prof.cpu_downscale_params_per_s) - 1 / (2 * b)
+        assert D.k_real_value(prof) == pytest.approx(float(num / den), rel=1e-12)
+        assert D.k_real_value(prof) == pytest.approx(frozen, rel=1e-12)
+        assert D.optimal_stride(prof).k == 2
+
+
+def test_all_cpu_sentinel():
+    assert repr(ALL_CPU) == "ALL_CPU"
+    assert copy.deepcopy(ALL_CPU) is ALL_CPU and pickle.loads(pickle.dumps(ALL_CPU)) is ALL_CPU
+    assert type(ALL_CPU)() is ALL_CPU
+    assert D.plan_stride_for(1) == 2 and D.plan_stride_for(ALL_CPU) is ALL_CPU
+    for bad in (0, 2.0):
+        with pytest.raises(ValueError):
+            D.plan_stride_for(bad)
+
+
+def _profile(**over):
+    base = dict(name="s", channel_params_per_s=3e9, fast_update_params_per_s=35e9, cpu_update_params_per_s=2e9,
+                cpu_downscale_params_per_s=8.7e9, fast_convert_bytes_per_s=1e12, host_convert_bytes_per_s=3e10,
+                host_alloc_bytes_per_s=4e9, pageable_d2h_bytes_per_s=6e9, pageable_h2d_bytes_per_s=5.5e9)
+    base.update(over)
+    return D.SystemProfile(**base)
+
+
+@given(b=st.floats(5e8, 5e10), u_g=st.floats(1e10, 2e11), u_c=st.floats(2e8, 2e10), d_c=st.floats(1e9, 5e10))
+@settings(max_examples=100, deadline=None)
+def test_integer_choice_is_exhaustive_argmin(b, u_g, u_c, d_c):
+    prof = _profile(channel_params_per_s=b, fast_update_params_per_s=u_g, cpu_update_params_per_s=u_c,
+                    cpu_downscale_params_per_s=d_c)
+    kr = D.k_real_value(prof)
+    if math.isinf(kr) or kr > 9.0 or abs(kr - round(kr)) < 0.15:
+        return
+    best = min(range(1, 12), key=lambda k: D.estimate_update_time(prof, 60, 10**7, k))
+    assert D.optimal_stride(prof).k == best
+
+
+def test_measured_b200_profile_accepts_infinite_downscale_rate():
+    prof = _profile(cpu_downscale_params_per_s=float("inf"))
+    assert math.isfinite(D.k_real_value(prof))
+    tl = D.simulate_update_phase(build_plan(6, 2), prof, 1000)
+    assert tl.makespan_ns > 0
+
+
+# ------------------------------------------------------------------ timing
+
+
+def test_sim_goldens():
+    bad = []
+    for key, want in SIM.items():
+        parts = key.split("|")
+        prof = D.get_profile(parts[0])
+        if parts[1] == "ragged":
+            tl = D.simulate_update_phase(build_plan(4, 2), prof, [1000, 1000, 1000, 500])
+            got = {"makespan": tl.makespan_ns, "events": sha(events_canon(tl.events))}
+        elif parts[1].startswith("cap"):
+            p2 = dataclasses.replace(prof, fast_capacity_bytes=12 * 1000 * int(parts[1][3:]))
+            tl = D.simulate_update_phase(build_plan(8, int(parts[2])), p2, 1000)
+            got = {"makespan": tl.makespan_ns, "span": tl.span_ns, "peak": tl.peak_fast_bytes,
+                   "events": sha(events_canon(tl.events))}
+        else:
+            n, s, r, pl, size = parts[1:]
+            tl = D.simulate_update_phase(build_plan(int(n), _stride(s), float(r), Placement(pl)), prof, int(size))
+            got = {"makespan": tl.makespan_ns, "span": tl.span_ns, "spill": tl.spillover_ns,
+                   "peak": tl.peak_fast_bytes, "events": sha(events_canon(tl.events)),
+                   "busy": {k.value: v for k, v in tl.lane_busy_ns.items()}}
+        if got != want:
+            bad.append(key)
+    assert not bad, bad[:10]
+
+
+def test_frozen_makespans(h100, v100):
+    tl = D.simulate_update_phase(build_plan(50, ALL_CPU), h100, 10**8)
+    assert (tl.makespan_ns, tl.span_ns) == (1_125_762_486, 1_129_398_850)
+    tl = D.simulate_update_phase(build_plan(50, 2), h100, 10**8)
+    assert (tl.makespan_ns, tl.spillover_ns) == (747_803_103, 19_015_153)
+    tl = D.simulate_update_phase(build_plan(1, ALL_CPU), v100, 10**8)
+    assert (tl.makespan_ns, tl.span_ns, tl.spillover_ns) == (61_494_253, 78_160_920, 16_666_667)
+
+
+def test_memory_trace_shapes(v100):
+    plan = build_plan(4, ALL_CPU)
+    assert D.memory_trace(D.simulate_update_phase(plan, v100, 1000).events, plan, 1000) == [(0, 16_000)]
+    plan = build_plan(6, 2)
+    trace = D.memory_trace(D.simulate_update_phase(plan, v100, 1000).events, plan, 1000)
+    assert trace[0][0] == 0 and trace[-1][1] == 24_000 and max(b for _, b in trace) >= 24_000 + 12_000
+
+
+def test_grad_flush_rates(h100):
+    host = D.grad_flush_throughput(D.GradFlushStrategy.FP16_HOST_UPSCALE, h100)
+    fast = D.grad_flush_throughput(D.GradFlushStrategy.GPU_UPSCALE_FP32, h100)
+    assert host == pytest.approx(2_731_277_533.04, rel=1e-6)
+    assert fast == pytest.approx(26_883_910_386.97, rel=1e-6)
+
+
+def test_sweep_orders_v100(v100):
+    res = D.sweep_stride(v100, 60, 10**8, k_values=[2, 3, 4, 5], jobs=2)
+    spans = [e.makespan_ns for e in res.entries]
+    assert spans == sorted(spans) and len(set(spans)) == 4
+    assert res.best_k == 2
