@@ -1,0 +1,410 @@
+#!/usr/bin/env python
+"""Update-phase benchmark (BASELINE.json metric: update-phase params/s and
+iteration time at 1/2/4/8 B200 vs the host-CPU reference).
+
+Workload at N=1: BASELINE.json configs[1] — a 7B-param (Llama-2-7B-sized)
+optimizer shard, fp32 Adam with bf16 grads and a bf16 working copy, 1e8-param
+subgroups, fp32 p/m/v homed in pinned host memory (host offload), the
+CPU/GPU interleave stride chosen by the performance model from constants
+measured on this box.  A step is one full update phase over the shard.
+Synthetic, seeded data generated on the device (no dataset exists).
+
+Under torchrun (N>1) the same 7B shard is ZeRO-3 partitioned across ranks
+(strong scaling); each rank runs its phase independently (the update needs
+no collective) and `value` is total params / max-over-ranks phase time.
+
+`--impl reference` times the reference's CPU implementation of the path —
+the oracle port (oracle/adam_oracle.c: the reference loop restated in C)
+with every host thread — on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "update-phase params/s and iteration time at 1/2/4/8 B200 vs host-CPU ref"
+UNIT = "params/s"
+BYTES_PER_PARAM_K1 = 28  # g(2) + p,m,v read (12) + p,m,v write (12) + bf16 copy (2)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--params", type=float, default=7e9)
+    ap.add_argument("--subgroup", type=float, default=1e8)
+    ap.add_argument("--lowp", default="bf16", choices=["bf16", "fp16"])
+    ap.add_argument("--stride", default="auto")
+    ap.add_argument("--static-ratio", type=float, default=0.0)
+    ap.add_argument("--capacity-gb", type=float, default=None,
+                    help="imposed dynamic fast-tier budget (default: two windows)")
+    ap.add_argument("--cpu-sample", type=int, default=3, help="subgroups timed for the CPU baseline")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile-out", default=None)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- helpers
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (clocks + throttle reasons)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def fill_shard(opt, seed: int, device) -> None:
+    """Seeded synthetic state generated on the device, subgroup by subgroup,
+    copied into the pinned host pool (numpy init of 7B would take ~10 min).
+    Distributions of core.py:259-272: p~N(0,.02), m~N(0,1e-3), v~U*1e-4, g~N(0,1)."""
+    import torch
+
+    gen = torch.Generator(device=device)
+    to_t = lambda a: torch.from_numpy(a.view(np.int16) if a.itemsize == 2 else a)
+    tdt = torch.bfloat16 if opt.lowp == "bf16" else torch.float16
+    for sg in opt.subgroups:
+        gen.manual_seed(seed * 1_000_003 + sg.index)
+        n, sl = sg.size, sg.slice
+        p = torch.randn(n, generator=gen, device=device) * 0.02
+        m = torch.randn(n, generator=gen, device=device) * 1e-3
+        v = torch.rand(n, generator=gen, device=device) * 1e-4
+        g = torch.randn(n, generator=gen, device=device).to(tdt)
+        to_t(opt._p[sl]).copy_(p)
+        to_t(opt._m[sl]).copy_(m)
+        to_t(opt._v[sl]).copy_(v)
+        to_t(opt._g[sl]).copy_(g.view(torch.int16))
+        to_t(opt._w[sl]).copy_(p.to(tdt).view(torch.int16))
+    torch.cuda.synchronize()
+
+
+def cpu_oracle_rate(sg: int, nsub: int, lowp: str, threads: int) -> dict:
+    """The oracle port (C restatement of the reference loop) on host cores."""
+    from oracle import c_oracle
+
+    c_oracle.build()
+    rng = np.random.default_rng(0)
+    p = (rng.standard_normal(sg, dtype=np.float32) * np.float32(0.02))
+    m = (rng.standard_normal(sg, dtype=np.float32) * np.float32(1e-3))
+    v = rng.random(sg, dtype=np.float32) * np.float32(1e-4)
+    g = (rng.standard_normal(sg, dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
+    w = np.empty(sg, dtype=np.uint16)
+    c_oracle.adam_mt(p, m, v, g, lowp, w, lowp, 1e-3, 0.9, 0.999, 1e-8, 1, nthreads=threads)  # warm
+    t0 = time.perf_counter()
+    for s in range(nsub):
+        c_oracle.adam_mt(p, m, v, g, lowp, w, lowp, 1e-3, 0.9, 0.999, 1e-8, 2 + s, nthreads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": nsub * sg / dt, "seconds": dt, "params": nsub * sg}
+
+
+# ---------------------------------------------------------------- reference arm
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    sg = int(args.subgroup)
+    nsub = max(1, args.cpu_sample)
+    for _ in range(args.warmup):
+        cpu_oracle_rate(sg, 1, args.lowp, threads)
+    vals, secs = [], 0.0
+    for _ in range(args.steps):
+        r = cpu_oracle_rate(sg, nsub, args.lowp, threads)
+        vals.append(r["value"])
+        secs += r["seconds"]
+    value = float(np.median(vals))
+    P = int(args.params)
+    sample = (f"{nsub} x {sg:.0e}-param subgroups per step (fused Adam + {args.lowp} working copy) of the "
+              f"{P / 1e9:g}B shard; full phase extrapolates to {P / value:.2f} s")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded)",
+        "config": {"workload": f"{P / 1e9:g}B-param Adam shard, {args.lowp} grads, sg={sg:.0e}, host cores only",
+                   "params": P, "subgroup": sg},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- B200 arm
+
+
+def main() -> None:
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2410_21316_b200 as D
+    from paper_2410_21316_b200 import profile_b200
+    from paper_2410_21316_b200.plan import ActionKind
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+        D._native.lib().dos_set_host_threads(max(1, len(os.sched_getaffinity(0)) // world))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    P = int(args.params)
+    SG = int(args.subgroup)
+    mine = D.shard(P, world, SG)[rank]
+    P_rank = sum(g.size for g in mine)
+    t_setup = time.perf_counter()
+    opt = D.ShardedOptimizer.allocate(P_rank, SG, lowp=args.lowp)
+    t_alloc = time.perf_counter() - t_setup
+    fill_shard(opt, seed=1234 + rank, device=device)
+    opt.to_device(device)
+    t_fill = time.perf_counter() - t_setup - t_alloc
+
+    cap = None if args.capacity_gb is None else int(args.capacity_gb * 1e9)
+    profile = profile_b200.measure_profile(fast_capacity_bytes=cap, quick=True)
+    nsg = len(opt.subgroups)
+    if args.stride == "auto":
+        choice = D.optimal_stride(profile, nsg, SG)
+        stride = choice.k
+    elif args.stride == "all_cpu":
+        stride, choice = D.ALL_CPU, None
+    else:
+        stride, choice = int(args.stride), None
+    plan = D.build_plan(nsg, stride, static_ratio=args.static_ratio)
+    hyper = D.AdamHyper()
+
+    for _ in range(args.warmup):
+        D.execute_plan(opt, plan, profile, hyper)
+    torch.cuda.synchronize()
+
+    # ---------------- timed region: device-resident grads (value)
+    clocks = ClockSampler(device.index)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    results = []
+    e0.record()
+    for _ in range(args.steps):
+        results.append(D.execute_plan(opt, plan, profile, hyper))
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    ms_max = max_over_ranks(ms)
+    value = P / (ms_max * 1e-3)
+
+    # per-step measured phase, K1 roofline from the measured GPU_UPDATE events
+    spans = [r.measured.span_ns for r in results]
+    makespans = [r.measured.makespan_ns for r in results]
+    k1_ns, k1_params, k1_launches = 0, 0, 0
+    h2d_b = d2h_b = 0
+    lane_busy = {}
+    for r in results:
+        for ev in r.measured.events:
+            a = ev.action
+            if a.kind is ActionKind.GPU_UPDATE:
+                k1_ns += ev.duration_ns
+                k1_params += opt.subgroups[a.subgroup].size
+                k1_launches += 1
+        for lane, b in r.measured.lane_busy_ns.items():
+            lane_busy[lane.value] = lane_busy.get(lane.value, 0) + b
+    for ev in results[0].timeline.events:
+        if ev.action.lane.value == "h2d":
+            h2d_b += ev.bytes
+        elif ev.action.lane.value == "d2h":
+            d2h_b += ev.bytes
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    k1_gbs = BYTES_PER_PARAM_K1 * k1_params / (k1_ns * 1e-9) / 1e9 if k1_ns else None
+    traffic = None
+    tf = ROOT / "profiles" / "k1_ncu_summary.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
+
+    # phase roofline: the slower of HBM time for the fast-tier params and the
+    # busier link direction at the measured per-direction rate (north_star)
+    link_Bps = profile.channel_params_per_s * 4.0
+    fast_params = sum(opt.subgroups[i].size for i, d in enumerate(plan.devices) if d is D.Device.FAST)
+    t_hbm = BYTES_PER_PARAM_K1 * fast_params / (hbm_peak * 1e9)
+    t_link = max(h2d_b, d2h_b) / link_Bps
+    t_host = (P_rank - fast_params) / profile.cpu_update_params_per_s
+    phase_ideal = max(t_hbm, t_link)
+
+    # ---------------- e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        tdt = torch.bfloat16 if args.lowp == "bf16" else torch.float16
+        res = opt.residency
+        fast_sgs = [g for i, g in enumerate(opt.subgroups) if plan.devices[i] is D.Device.FAST]
+        host_g = torch.from_numpy(opt._g.view(np.int16))
+        host_w = torch.from_numpy(opt._w.view(np.int16))
+        dev_g = res.grads.view(torch.int16)
+        dev_w = res.model16.view(torch.int16)
+        h2d_e2e = sum(2 * g.size for g in fast_sgs)
+        d2h_e2e = h2d_e2e
+        barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(args.steps):
+            for g in fast_sgs:  # the step's grads arrive from pinned host memory
+                dev_g[g.slice].copy_(host_g[g.slice], non_blocking=True)
+            D.execute_plan(opt, plan, profile, hyper)
+            for g in fast_sgs:  # the device-updated working copy back to the host image
+                host_w[g.slice].copy_(dev_w[g.slice], non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        f1.record()
+        torch.cuda.synchronize()
+        barrier()
+        e2e_ms = max_over_ranks(f0.elapsed_time(f1) / args.steps)
+        e2e = {"value": P / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d_e2e * world,
+               "d2h_bytes_per_step": d2h_e2e * world, "ms_per_step": e2e_ms}
+
+    # ---------------- CPU baseline: the oracle port on host cores (rank 0, N=1)
+    cpu_baseline = None
+    if rank == 0 and world == 1:
+        threads = len(os.sched_getaffinity(0))
+        r = cpu_oracle_rate(SG, args.cpu_sample, args.lowp, threads)
+        cpu_baseline = {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "port",
+                        "sample": f"{args.cpu_sample} x {SG:.0e}-param subgroups ({r['seconds']:.1f} s), "
+                                  f"oracle/adam_oracle.c with {threads} threads"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_max,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic (seeded, generated on device)",
+            "config": {
+                "workload": f"{P / 1e9:g}B-param fp32 Adam shard, {args.lowp} grads + working copy, "
+                            f"host offload (BASELINE configs[1])",
+                "params": P, "subgroup": SG, "subgroups_per_rank": nsg, "lowp": args.lowp,
+                "stride": "all_cpu" if stride is D.ALL_CPU else stride,
+                "k_real": None if choice is None else choice.k_real,
+                "static_ratio": args.static_ratio, "fast_capacity_bytes": cap, "hbm_windows": results[0].measured and
+                min(2, 2 if cap is None else cap // (12 * SG)),
+                "parallelism": f"zero3-shard{world}", "l2": "inputs > L2 (28 B/param over 1e8-param subgroups)",
+            },
+            "iteration": {
+                "update_span_ms_median": float(np.median(spans)) / 1e6,
+                "update_makespan_ms_median": float(np.median(makespans)) / 1e6,
+                "predicted_makespan_ms": results[0].timeline.makespan_ns / 1e6,
+                "predicted_span_ms": results[0].timeline.span_ns / 1e6,
+                "lane_busy_ms_per_step": {k: v / 1e6 / len(results) for k, v in lane_busy.items()},
+                "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
+            },
+            "roofline": {"bound": "hbm", "achieved": k1_gbs, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": (k1_gbs / hbm_peak) if k1_gbs else None, "traffic": traffic,
+                         "kernel": "K1 dos_adam (fused Adam + bf16 copy)",
+                         "bytes_per_param": BYTES_PER_PARAM_K1, "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+            "phase_roofline": {
+                "bound": "link" if t_link >= t_hbm else "hbm",
+                "ideal_ms": phase_ideal * 1e3, "achieved_ms": ms_max, "frac": phase_ideal * 1e3 / ms_max,
+                "link_GBs_per_dir_measured": link_Bps / 1e9, "host_update_ms_at_measured_rate": t_host * 1e3,
+            },
+            "cpu_baseline": cpu_baseline,
+            "e2e": e2e,
+            "gpu_launches": k1_launches,
+            "clocks": clk,
+            "profile": {"channel_params_per_s": profile.channel_params_per_s,
+                        "fast_update_params_per_s": profile.fast_update_params_per_s,
+                        "cpu_update_params_per_s": profile.cpu_update_params_per_s,
+                        "host_contention": profile.host_contention,
+                        "host_threads": D._native.lib().dos_host_threads()},
+            "setup_s": {"alloc_pin": t_alloc, "fill": t_fill},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

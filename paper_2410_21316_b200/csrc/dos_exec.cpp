@@ -249,11 +249,29 @@ struct Engine {
 
     cudaStream_t s = a->lane == DOS_LANE_FAST ? st[0] : a->lane == DOS_LANE_H2D ? st[1] : st[2];
     int rc = gpu_wait_deps(s, a);
+    if (rc == DOS_OK && a->kind == DOS_PREFETCH_M && !a->is_static && sg_slot[sg] < 0) rc = open_window(sg, s);
     if (rc != DOS_OK) return fail(rc, dos_last_error());
     DOS_CU(cudaEventRecord(ev_s[a->id], s));
     rc = enqueue_gpu(a, s);
     if (rc != DOS_OK) return fail(rc, dos_last_error());
     DOS_CU(cudaEventRecord(ev_e[a->id], s));
+    return DOS_OK;
+  }
+
+  // A window opens at PREFETCH_M: take the next physical slot and make the
+  // stream wait for the flush that released it (before the start stamp).
+  int open_window(int sg, cudaStream_t s) {
+    const int sl = next_slot;
+    if (slot_release[sl] == -2)
+      return dos_set_error(DOS_EINFEASIBLE, "subgroup %d opens a window while slot %d (subgroup %d) is still unflushed",
+                           sg, sl, slot_owner[sl]);
+    if ((int64_t)sg_size[sg] > slot_elems)
+      return dos_set_error(DOS_EINFEASIBLE, "subgroup %d (%lld) exceeds the HBM window", sg, (long long)sg_size[sg]);
+    if (slot_release[sl] >= 0) DOS_CU(cudaStreamWaitEvent(s, ev_e[slot_release[sl]], 0));
+    next_slot = (sl + 1) % nslots;
+    slot_release[sl] = -2;
+    slot_owner[sl] = sg;
+    sg_slot[sg] = sl;
     return DOS_OK;
   }
 
@@ -270,19 +288,7 @@ struct Engine {
         if (a->is_static) return dos_set_error(DOS_ESTATE, "static subgroup %d prefetched", sg);
         const int piece = a->kind == DOS_PREFETCH_M ? PIECE_M : a->kind == DOS_PREFETCH_V ? PIECE_V : PIECE_P;
         if (n > slot_elems) return dos_set_error(DOS_EINFEASIBLE, "subgroup %d (%lld) exceeds the HBM window", sg, (long long)n);
-        if (sg_slot[sg] < 0) {
-          // window opens: take the next physical slot
-          const int sl = next_slot;
-          if (slot_release[sl] == -2)
-            return dos_set_error(DOS_EINFEASIBLE,
-                                 "subgroup %d opens a window while slot %d (subgroup %d) is still unflushed", sg, sl,
-                                 slot_owner[sl]);
-          if (slot_release[sl] >= 0) DOS_CU(cudaStreamWaitEvent(s, ev_e[slot_release[sl]], 0));
-          next_slot = (sl + 1) % nslots;
-          slot_release[sl] = -2;
-          slot_owner[sl] = sg;
-          sg_slot[sg] = sl;
-        }
+        if (sg_slot[sg] < 0) return dos_set_error(DOS_ESTATE, "subgroup %d prefetched before its window opened", sg);
         if (sg_mask[sg] & (1u << piece))
           return dos_set_error(DOS_ESTATE, "subgroup %d piece %c staged twice", sg, "mvp"[piece]);
         sg_mask[sg] |= (uint8_t)(1u << piece);

@@ -1,0 +1,199 @@
+"""Measure the ``b200-node`` SystemProfile on the machine at hand.
+
+The performance model (Eq. 1) is only as good as its constants; the
+reference ships hand-entered V100/H100 numbers (catalog.py:23-51).  Here
+every constant the planner uses is measured on the B200 box, quickly enough
+to re-fit per iteration:
+
+* ``channel_params_per_s``       pinned H2D and D2H run *concurrently*
+                                 (duplex, as in the interleaved phase), the
+                                 slower direction / 4 B per fp32 param;
+* ``fast_update_params_per_s``   K1 on one subgroup resident in HBM;
+* ``cpu_update_params_per_s``    H1 (fused Adam + working-copy store) on the
+                                 host team, while the link is busy (the
+                                 contended rate, which is what the phase sees);
+* ``cpu_downscale_params_per_s`` inf: the downscale is fused into H1;
+* ``host_contention``            H1 alone / H1 under concurrent DMA (>= 1).
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import json
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+from . import _native as N
+from .state import SystemProfile
+
+_OUT = Path(__file__).resolve().parent.parent / "profiles" / "b200_node_profile.json"
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def measure_link(nbytes: int = 1 << 30, reps: int = 3) -> dict:
+    """Pinned host<->device GB/s: each direction alone and both at once."""
+    torch = _torch()
+    dev = torch.device("cuda")
+    hb1 = N.HostBuffer(nbytes)
+    hb2 = N.HostBuffer(nbytes)
+    h1 = torch.from_numpy(hb1.array(np.uint8, nbytes))
+    h2 = torch.from_numpy(hb2.array(np.uint8, nbytes))
+    d1 = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(fn) -> float:
+        fn()
+        torch.cuda.synchronize()
+        best = float("inf")
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            best = min(best, time.perf_counter() - t0)
+        return best
+
+    def h2d():
+        with torch.cuda.stream(s1):
+            d1.copy_(h1, non_blocking=True)
+
+    def d2h():
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+
+    t_h2d = timed(h2d)
+    t_d2h = timed(d2h)
+    t_dup = timed(lambda: (h2d(), d2h()))
+    return {"h2d_GBs": nbytes / t_h2d / 1e9, "d2h_GBs": nbytes / t_d2h / 1e9,
+            "duplex_GBs_per_dir": nbytes / t_dup / 1e9}
+
+
+def measure_k1(n: int = 100_000_000, reps: int = 5) -> dict:
+    """K1 params/s and achieved HBM GB/s (28 B/param) on one subgroup."""
+    torch = _torch()
+    dev = torch.device("cuda")
+    p = torch.randn(n, device=dev) * 0.02
+    m = torch.randn(n, device=dev) * 1e-3
+    v = torch.rand(n, device=dev) * 1e-4
+    g = torch.randn(n, device=dev).to(torch.bfloat16)
+    w = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    sc = N.scalars(1e-3, 0.9, 0.999, 1e-8, np.float32(0.1), np.float32(0.001))
+    st = torch.cuda.current_stream()
+    lib = N.lib()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def run():
+        N.check(lib.dos_adam_step_cuda(p.data_ptr(), m.data_ptr(), v.data_ptr(), g.data_ptr(), N.DOS_BF16,
+                                       w.data_ptr(), N.DOS_BF16, n, sc, st.cuda_stream))
+
+    for _ in range(3):
+        run()
+    times = []
+    for _ in range(reps):
+        e0.record(st)
+        run()
+        e1.record(st)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1) * 1e-3)
+    t = float(np.median(times))
+    return {"k1_params_per_s": n / t, "k1_GBs": 28 * n / t / 1e9, "k1_ms": t * 1e3, "n": n}
+
+
+def measure_h1(n: int = 100_000_000, with_dma: bool = False, reps: int = 3) -> dict:
+    """H1 params/s (fused Adam + bf16 store) on the host team."""
+    hb = N.HostBuffer(n * 16)
+    p = hb.array(np.float32, n, 0)
+    m = hb.array(np.float32, n, 4 * n)
+    v = hb.array(np.float32, n, 8 * n)
+    g = hb.array(np.uint16, n, 12 * n)
+    w = hb.array(np.uint16, n, 14 * n)
+    rng = np.random.default_rng(0)
+    p[:] = rng.standard_normal(n, dtype=np.float32) * np.float32(0.02)
+    m[:] = 0
+    v[:] = np.float32(1e-5)
+    g[:] = 0x3F80
+    sc = N.scalars(1e-3, 0.9, 0.999, 1e-8, np.float32(0.1), np.float32(0.001))
+    lib = N.lib()
+    stop = threading.Event()
+    dma = None
+    if with_dma:
+        torch = _torch()
+        nb = 1 << 29
+        hx = torch.from_numpy(N.HostBuffer(nb).array(np.uint8, nb))
+        hy = torch.from_numpy(N.HostBuffer(nb).array(np.uint8, nb))
+        dx = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        dy = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+        def pump():
+            while not stop.is_set():
+                with torch.cuda.stream(s1):
+                    dx.copy_(hx, non_blocking=True)
+                with torch.cuda.stream(s2):
+                    hy.copy_(dy, non_blocking=True)
+                s1.synchronize()
+                s2.synchronize()
+
+        dma = threading.Thread(target=pump, daemon=True)
+        dma.start()
+        time.sleep(0.05)
+    run = lambda: N.check(lib.dos_adam_step_host(p.ctypes.data, m.ctypes.data, v.ctypes.data, g.ctypes.data,
+                                                  N.DOS_BF16, w.ctypes.data, N.DOS_BF16, n, sc, 0))
+    run()
+    best = float("inf")
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        run()
+        best = min(best, time.perf_counter() - t0)
+    if dma is not None:
+        stop.set()
+        dma.join()
+    return {"h1_params_per_s": n / best, "h1_GBs": 28 * n / best / 1e9, "threads": lib.dos_host_threads()}
+
+
+def measure_profile(fast_capacity_bytes: int | None = None, save: bool = False, quick: bool = False) -> SystemProfile:
+    """Measure all planner constants on this box; returns a SystemProfile."""
+    n = 25_000_000 if quick else 100_000_000
+    link = measure_link(1 << 28 if quick else 1 << 30)
+    k1 = measure_k1(n)
+    h1_alone = measure_h1(n)
+    h1_busy = measure_h1(n, with_dma=True)
+    channel = min(link["duplex_GBs_per_dir"], link["h2d_GBs"], link["d2h_GBs"]) * 1e9 / 4.0
+    contention = max(1.0, h1_alone["h1_params_per_s"] / h1_busy["h1_params_per_s"])
+    prof = SystemProfile(
+        name="b200-node",
+        channel_params_per_s=channel,
+        fast_update_params_per_s=k1["k1_params_per_s"],
+        cpu_update_params_per_s=h1_alone["h1_params_per_s"],
+        cpu_downscale_params_per_s=float("inf"),
+        fast_convert_bytes_per_s=2.0 * k1["k1_params_per_s"],
+        host_convert_bytes_per_s=2.0 * h1_alone["h1_params_per_s"],
+        host_alloc_bytes_per_s=4e9,
+        pageable_d2h_bytes_per_s=link["d2h_GBs"] * 1e9 / 3.0,
+        pageable_h2d_bytes_per_s=link["h2d_GBs"] * 1e9 / 5.0,
+        fast_capacity_bytes=fast_capacity_bytes,
+        host_contention=contention,
+        caveat="measured by profile_b200.measure_profile",
+    )
+    if save:
+        d = dataclasses.asdict(prof)
+        d["raw"] = {"link": link, "k1": k1, "h1_alone": h1_alone, "h1_with_dma": h1_busy,
+                    "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
+        _OUT.parent.mkdir(exist_ok=True)
+        _OUT.write_text(json.dumps(d, indent=1))
+    return prof
+
+
+if __name__ == "__main__":
+    import sys
+
+    prof = measure_profile(save="--save" in sys.argv, quick="--quick" in sys.argv)
+    print(json.dumps(dataclasses.asdict(prof), indent=1))
