@@ -130,6 +130,12 @@ typedef struct dos_state_desc {
   float* dev_static_p;
   float* dev_static_m;
   float* dev_static_v;
+  /* host_io != 0: the step's grads arrive in host_g for every subgroup and
+   * the working copy must also land in host_lowp.  Fast subgroups then copy
+   * their grads H2D inside PREFETCH_P (static: inside GPU_UPDATE, before K1)
+   * and their working copy D2H inside FLUSH_OUT_P (static: inside
+   * FLUSH_OUT_MODEL16), so the extra 2+2 B/param ride the same lanes. */
+  int32_t host_io;
 } dos_state_desc;
 
 typedef struct dos_exec_config {

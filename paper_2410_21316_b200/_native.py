@@ -54,6 +54,7 @@ class dos_state_desc(C.Structure):
         ("host_g", C.c_void_p), ("host_lowp", C.c_void_p),
         ("dev_g", C.c_void_p), ("dev_lowp", C.c_void_p),
         ("dev_static_p", C.c_void_p), ("dev_static_m", C.c_void_p), ("dev_static_v", C.c_void_p),
+        ("host_io", C.c_int32),
     ]
 
 

@@ -275,6 +275,16 @@ struct Engine {
     return DOS_OK;
   }
 
+  // host_io transfers (see dos_state_desc.host_io)
+  cudaError_t copy_grads_h2d(int64_t start, int64_t n, cudaStream_t s) {
+    return cudaMemcpyAsync(static_cast<char*>(const_cast<void*>(S.dev_g)) + 2 * start,
+                           static_cast<const char*>(S.host_g) + 2 * start, (size_t)n * 2, cudaMemcpyHostToDevice, s);
+  }
+  cudaError_t copy_lowp_d2h(int64_t start, int64_t n, cudaStream_t s) {
+    return cudaMemcpyAsync(static_cast<char*>(S.host_lowp) + 2 * start, static_cast<const char*>(S.dev_lowp) + 2 * start,
+                           (size_t)n * 2, cudaMemcpyDeviceToHost, s);
+  }
+
   int enqueue_gpu(const dos_action_desc* a, cudaStream_t s) {
     const int sg = a->subgroup;
     const int64_t start = sg_start[sg], n = sg_size[sg];
@@ -294,6 +304,7 @@ struct Engine {
         sg_mask[sg] |= (uint8_t)(1u << piece);
         const float* src = (piece == PIECE_M ? S.host_m : piece == PIECE_V ? S.host_v : S.host_p) + start;
         DOS_CU(cudaMemcpyAsync(slot_ptr(sg_slot[sg], piece), src, (size_t)n * 4, cudaMemcpyHostToDevice, s));
+        if (S.host_io && piece == PIECE_P) DOS_CU(copy_grads_h2d(start, n, s));
         return DOS_OK;
       }
       case DOS_GPU_UPDATE: {
@@ -302,6 +313,7 @@ struct Engine {
         if (a->is_static) {
           const int64_t o = static_off[sg];
           if (o < 0) return dos_set_error(DOS_ESTATE, "subgroup %d marked static but has no HBM residence", sg);
+          if (S.host_io) DOS_CU(copy_grads_h2d(start, n, s));
           return dos_adam_launch(S.dev_static_p + o, S.dev_static_m + o, S.dev_static_v + o, g, lt, lp, lt, n, K, s);
         }
         if (sg_slot[sg] < 0 || sg_mask[sg] != 7u)
@@ -315,6 +327,7 @@ struct Engine {
         // K1 already stored the working copy in the same pass.
         if (!a->is_static && !(sg_slot[sg] >= 0 && (sg_mask[sg] & (1u << PIECE_P))))
           return dos_set_error(DOS_ESTATE, "FLUSH_OUT_MODEL16 of subgroup %d without staged params", sg);
+        if (S.host_io && a->is_static) DOS_CU(copy_lowp_d2h(start, n, s));
         return DOS_OK;
       case DOS_FLUSH_OUT_M:
       case DOS_FLUSH_OUT_V:
@@ -325,6 +338,7 @@ struct Engine {
         float* dst = (piece == PIECE_M ? S.host_m : piece == PIECE_V ? S.host_v : S.host_p) + start;
         const int sl = sg_slot[sg];
         DOS_CU(cudaMemcpyAsync(dst, slot_ptr(sl, piece), (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+        if (S.host_io && piece == PIECE_P) DOS_CU(copy_lowp_d2h(start, n, s));
         sg_mask[sg] &= (uint8_t)~(1u << piece);
         if (sg_mask[sg] == 0) {  // window closes with this flush
           slot_release[sl] = a->id;

@@ -158,8 +158,9 @@ class DeviceResidency:
         else:
             self.static_p = self.static_m = self.static_v = None
 
-    def after_phase(self) -> None:
-        self.host_stale.add("_w")
+    def after_phase(self, host_io: bool = False) -> None:
+        if not host_io:  # with host_io the engine mirrored the working copy to the host
+            self.host_stale.add("_w")
         if self.static_set:
             self.host_stale.update(("_p", "_m", "_v"))
 
@@ -176,7 +177,7 @@ class DeviceResidency:
             self._engines[key] = eng
         return eng
 
-    def state_desc(self) -> tuple[N.dos_state_desc, list]:
+    def state_desc(self, host_io: bool = False) -> tuple[N.dos_state_desc, list]:
         opt = self.opt
         keep = [self.sg_start, self.sg_size, self.static_off]
         p64 = C.POINTER(C.c_int64)
@@ -192,6 +193,7 @@ class DeviceResidency:
             dev_static_p=self.static_p.data_ptr() if self.static_p is not None else None,
             dev_static_m=self.static_m.data_ptr() if self.static_m is not None else None,
             dev_static_v=self.static_v.data_ptr() if self.static_v is not None else None,
+            host_io=1 if host_io else 0,
         )
         return d, keep
 
@@ -282,7 +284,8 @@ class B200Target(SimTarget):
     """
 
     def __init__(self, profile: SystemProfile, plan: UpdatePlan, optimizer: ShardedOptimizer, hyper,
-                 step: int, *, host_threads: int = 0, fuse_downscale: bool = True) -> None:
+                 step: int, *, host_threads: int = 0, fuse_downscale: bool = True,
+                 host_io: bool = False) -> None:
         sizes = tuple(g.size for g in optimizer.subgroups)
         super().__init__(profile, plan, sizes)
         self.opt = optimizer
@@ -293,11 +296,12 @@ class B200Target(SimTarget):
         self.num_slots, slot_elems = slots_for(profile, plan, sizes)
         self.engine = self.residency.engine(self.num_slots, slot_elems, host_threads, fuse_downscale)
         self._descs = plan_descs(plan)
+        self.host_io = host_io
         self._begun = False
         self._submitted = 0
 
     def _begin(self) -> None:
-        desc, keep = self.residency.state_desc()
+        desc, keep = self.residency.state_desc(self.host_io)
         self._keep = (desc, keep)
         h = self.hyper
         bc1, bc2 = bias_corrections(h.beta1, h.beta2, self.step)

@@ -1,0 +1,157 @@
+"""ZeRO-3 data parallelism around the update phase.
+
+One process per GPU.  Rank r owns ``shard(P, N, SG)[r]`` (core.py:139-170):
+its fp32 optimizer state, its grads and its slice of the working copy.  The
+update phase itself is rank-local — no collective on the
+data path.  Around it:
+
+* before: **reduce-scatter** of the bf16 grads, bucketed per subgroup index
+  j (bucket j = every rank's subgroup j; each rank receives its own), so the
+  phase can start on bucket 0 while later buckets are still reducing;
+* after: **all-gather** of the bf16 working copy, bucketed the same way.
+  ``gather_params_overlapped`` makes a comm stream wait on the *engine event*
+  of the action that finalises subgroup j's working copy (its GPU_UPDATE, or
+  its H2D_PARAMS16 for a host subgroup) and launches bucket j's all-gather
+  right away, so gathers overlap the rest of the phase.
+
+Full-model buffers use the model's flat (rank-major) layout padded to
+``N * ceil(P/N)``; the last rank's missing tail is zero padding so every
+collective has equal counts.  NCCL over NVLink/NVSwitch is the product
+backend; the same code runs on gloo (CPU tests), where reduce-scatter is
+emulated by all-reduce + slice.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+from .state import Subgroup, shard
+
+
+@dataclass(frozen=True)
+class ShardLayout:
+    """Where every rank's subgroups live in the padded full-model buffer."""
+
+    total_params: int
+    world: int
+    subgroup_size: int
+    per_rank: int  # ceil(P / N): every rank's padded share
+    ranks: tuple[tuple[Subgroup, ...], ...]
+
+    @classmethod
+    def build(cls, total_params: int, world: int, subgroup_size: int) -> "ShardLayout":
+        parts = shard(total_params, world, subgroup_size)
+        return cls(total_params, world, subgroup_size, math.ceil(total_params / world),
+                   tuple(tuple(p) for p in parts))
+
+    @property
+    def padded_total(self) -> int:
+        return self.per_rank * self.world
+
+    @property
+    def num_buckets(self) -> int:
+        """Bucket count: subgroups of the fullest rank (rank 0)."""
+        return len(self.ranks[0])
+
+    def bucket_span(self, j: int) -> tuple[int, int]:
+        """(start, size) of bucket j inside one rank's padded share; the size
+        is rank 0's subgroup j (padding covers shorter ranks)."""
+        sg = self.ranks[0][j]
+        return sg.start, sg.size
+
+    def global_offset(self, rank: int, local_start: int) -> int:
+        return rank * self.per_rank + local_start
+
+    def rank_of_bucket_piece(self, rank: int, j: int) -> tuple[int, int]:
+        """(valid elements, padding) of rank's piece of bucket j."""
+        start, size = self.bucket_span(j)
+        mine = sum(g.size for g in self.ranks[rank])
+        valid = max(0, min(size, mine - start))
+        return valid, size - valid
+
+
+class BucketedCollectives:
+    """Bucketed reduce-scatter / all-gather over a torch process group."""
+
+    def __init__(self, layout: ShardLayout, group=None) -> None:
+        import torch.distributed as dist
+
+        self.layout = layout
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if self.world != layout.world:
+            raise ValueError(f"layout is for {layout.world} ranks, group has {self.world}")
+        self.backend = dist.get_backend(group)
+
+    def _views(self, full, j):
+        start, size = self.layout.bucket_span(j)
+        return [full[self.layout.global_offset(r, start): self.layout.global_offset(r, start) + size]
+                for r in range(self.world)]
+
+    def reduce_scatter_bucket(self, full_grads, out, j: int, op=None):
+        """Sum bucket j of every rank's full-model grads into ``out`` (this
+        rank's piece of bucket j, length = bucket size)."""
+        import torch
+        import torch.distributed as dist
+
+        op = dist.ReduceOp.SUM if op is None else op
+        views = self._views(full_grads, j)
+        if self.backend == "nccl":
+            return dist.reduce_scatter(out, views, op=op, group=self.group, async_op=True)
+        # gloo: no reduce-scatter; all-reduce the bucket and keep our piece
+        buf = torch.cat(views)
+        dist.all_reduce(buf, op=op, group=self.group)
+        size = views[0].numel()
+        out.copy_(buf[self.rank * size:(self.rank + 1) * size])
+        return None
+
+    def all_gather_bucket(self, full_params, mine, j: int):
+        """Every rank's piece of bucket j into the full-model buffer."""
+        import torch.distributed as dist
+
+        views = self._views(full_params, j)
+        if self.backend == "nccl":
+            return dist.all_gather(views, mine, group=self.group, async_op=True)
+        dist.all_gather(views, mine.contiguous(), group=self.group)
+        return None
+
+    def reduce_scatter_all(self, full_grads, shard_grads, scale: float | None = None):
+        """All buckets; ``shard_grads`` is this rank's padded share (per_rank)."""
+        works = []
+        for j in range(self.layout.num_buckets):
+            start, size = self.layout.bucket_span(j)
+            works.append(self.reduce_scatter_bucket(full_grads, shard_grads[start:start + size], j))
+        for w in works:
+            if w is not None:
+                w.wait()
+        if scale is not None:
+            shard_grads.mul_(scale)
+
+    def all_gather_all(self, full_params, shard_params):
+        works = []
+        for j in range(self.layout.num_buckets):
+            start, size = self.layout.bucket_span(j)
+            works.append(self.all_gather_bucket(full_params, shard_params[start:start + size], j))
+        for w in works:
+            if w is not None:
+                w.wait()
+
+
+def finalising_actions(plan) -> dict[int, int]:
+    """Subgroup -> id of the device action after which its working copy is final.
+
+    Fast subgroups: their GPU_UPDATE (K1 stores the working copy).  Host
+    subgroups: their H2D_PARAMS16.  Every one is a device-lane action, so
+    the engine holds a CUDA event for it.
+    """
+    from .plan import ActionKind, Device
+
+    out: dict[int, int] = {}
+    for a in plan.actions:
+        if a.kind is ActionKind.GPU_UPDATE:
+            out[a.subgroup] = a.id
+        elif a.kind is ActionKind.H2D_PARAMS16 and plan.devices[a.subgroup] is Device.CPU:
+            out[a.subgroup] = a.id
+    return out

@@ -168,6 +168,7 @@ def execute_plan(
     throttle_scale: float = 1e-3,
     *,
     host_threads: int = 0,
+    host_io: bool = False,
     check_coherence: bool = False,
     validate_measured: bool = True,
 ) -> ExecutionResult:
@@ -178,13 +179,19 @@ def execute_plan(
     drain, bumps ``step``.  ``check_coherence`` re-derives the working copy
     from the fp32 params and compares bitwise (the reference always does;
     here it is opt-in because it is a full extra pass).
+
+    ``host_io=True`` is the host-buffer mode: this step's gradients are read
+    from the host image (``grads16``) for every subgroup — fast subgroups
+    ship theirs H2D inside their prefetch — and the working copy is mirrored
+    into the host ``model16`` inside the flushes, so both host images are
+    coherent when the call returns.
     """
     if plan.num_subgroups != len(optimizer.subgroups):
         raise ValueError(f"plan covers {plan.num_subgroups} subgroups, optimizer has {len(optimizer.subgroups)}")
     if mode is ExecMode.THROTTLED and throttle_scale <= 0:
         raise ValueError("throttle_scale must be positive")
     step = optimizer.step + 1
-    target = B200Target(profile, plan, optimizer, hyper, step, host_threads=host_threads)
+    target = B200Target(profile, plan, optimizer, hyper, step, host_threads=host_threads, host_io=host_io)
     try:
         events = run_update(plan, target)
     except BaseException:
@@ -192,7 +199,7 @@ def execute_plan(
         raise
     measured_events = target.finish()
     validate_schedule(plan, events, target)
-    target.residency.after_phase()
+    target.residency.after_phase(host_io)
     sizes = target.sizes
     measured = build_timeline(plan, measured_events, sizes) if measured_events else None
     if validate_measured and measured_events:

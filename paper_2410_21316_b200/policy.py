@@ -1,0 +1,120 @@
+"""Per-iteration re-fit of the performance model and the B200 stride policy.
+
+The reference's planner (``optimal_stride``, perfmodel.py:155-179) is kept
+bit-identical in ``perfmodel``; this module adds what the north star asks of
+the B200 build: constants re-derived from the *measured* timeline of the
+previous iteration, and a split chosen per iteration.
+
+``simulate_b200_phase`` is the reference list scheduler (scheduler.py:
+402-466) with the two rules the B200 engine changes: state streams are not
+FIFO across directions (each in-flight window has its own HBM slot), and a
+window opens only when the window ``num_slots`` earlier has fully flushed.
+FLUSH_OUT_MODEL16 and CPU_DOWNSCALE cost nothing (fused into K1 / H1).
+``choose_stride`` takes the candidate with the smallest predicted span.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+from typing import Iterable, Sequence
+
+from .perfmodel import ALL_CPU
+from .plan import ActionKind, Device, Lane, UpdatePlan, build_plan
+from .state import SystemProfile
+from .timing import SimTarget, Timeline, build_timeline, normalize_sizes
+
+_H2D_STATE = (ActionKind.PREFETCH_M, ActionKind.PREFETCH_V, ActionKind.PREFETCH_P)
+_D2H_STATE = (ActionKind.FLUSH_OUT_M, ActionKind.FLUSH_OUT_V, ActionKind.FLUSH_OUT_P)
+
+
+def refit_profile(profile: SystemProfile, measured: Timeline, sizes: Sequence[int]) -> SystemProfile:
+    """Rates observed in a measured phase, folded into ``profile``.
+
+    link: bytes / busy time of each direction's fp32 state copies (slower
+    direction); K1: params / GPU_UPDATE time; host: params / CPU_UPDATE time,
+    which was measured *under* link traffic, so the uncontended rate stored
+    is that times ``host_contention``.
+    """
+    acc = {"h2d": [0, 0], "d2h": [0, 0], "gpu": [0, 0], "cpu": [0, 0]}
+    for ev in measured.events:
+        a, d = ev.action, ev.duration_ns
+        if d <= 0:
+            continue
+        if a.kind in _H2D_STATE:
+            acc["h2d"][0] += sizes[a.subgroup]
+            acc["h2d"][1] += d
+        elif a.kind in _D2H_STATE:
+            acc["d2h"][0] += sizes[a.subgroup]
+            acc["d2h"][1] += d
+        elif a.kind is ActionKind.GPU_UPDATE:
+            acc["gpu"][0] += sizes[a.subgroup]
+            acc["gpu"][1] += d
+        elif a.kind is ActionKind.CPU_UPDATE:
+            acc["cpu"][0] += sizes[a.subgroup]
+            acc["cpu"][1] += d
+    rate = {k: (n / (t * 1e-9) if t else None) for k, (n, t) in acc.items()}
+    upd = {}
+    links = [r for r in (rate["h2d"], rate["d2h"]) if r]
+    if links:
+        upd["channel_params_per_s"] = min(links)
+    if rate["gpu"]:
+        upd["fast_update_params_per_s"] = rate["gpu"]
+    if rate["cpu"]:
+        upd["cpu_update_params_per_s"] = rate["cpu"] * profile.host_contention
+    return dataclasses.replace(profile, **upd)
+
+
+class _B200Durations(SimTarget):
+    """SimTarget durations with the B200's fused actions made free."""
+
+    def duration_ns(self, action) -> int:
+        if action.kind in (ActionKind.FLUSH_OUT_MODEL16, ActionKind.CPU_DOWNSCALE):
+            return 0
+        return super().duration_ns(action)
+
+
+def simulate_b200_phase(plan: UpdatePlan, profile: SystemProfile, subgroup_size: "int | Sequence[int]",
+                        num_slots: int = 2) -> Timeline:
+    """Predicted timeline of ``plan`` on the B200 engine (see module doc)."""
+    sizes = normalize_sizes(plan, subgroup_size)
+    t = _B200Durations(profile, plan, sizes)
+    lane_free = dict.fromkeys(Lane, 0)
+    finish: list[int] = []
+    closes: list[int] = []  # window close times in opening order
+    dyn = set(plan.dynamic_fast)
+    from .plan import ScheduledAction
+
+    out = []
+    for a in plan.actions:
+        start = max([lane_free[a.lane], *(finish[d] for d in a.deps)])
+        if a.kind is ActionKind.PREFETCH_M and a.subgroup in dyn:
+            opened = len(closes)
+            if opened >= num_slots:
+                start = max(start, closes[opened - num_slots])
+            closes.append(-1)  # filled at FLUSH_OUT_P
+            t._win = getattr(t, "_win", {})
+            t._win[a.subgroup] = opened
+        end = start + t.duration_ns(a)
+        finish.append(end)
+        lane_free[a.lane] = end
+        if a.kind is ActionKind.FLUSH_OUT_P and a.subgroup in dyn:
+            closes[t._win[a.subgroup]] = end
+        out.append(ScheduledAction(action=a, start_ns=start, end_ns=end, bytes=t.bytes_of(a)))
+    return build_timeline(plan, tuple(out), sizes)
+
+
+def choose_stride(profile: SystemProfile, sizes: Sequence[int], candidates: Iterable = range(1, 7),
+                  static_ratio: float = 0.0, num_slots: int = 2):
+    """Stride with the smallest predicted B200 span; returns (stride, {stride: span_ns})."""
+    n = len(sizes)
+    spans = {}
+    for k in candidates:
+        plan = build_plan(n, k, static_ratio=static_ratio)
+        spans[k] = simulate_b200_phase(plan, profile, list(sizes), num_slots).span_ns
+    best = min(spans, key=lambda k: (spans[k], 0 if k is ALL_CPU else k))
+    return best, spans
+
+
+def fast_fraction(plan: UpdatePlan, sizes: Sequence[int]) -> float:
+    tot = sum(sizes)
+    return sum(s for i, s in enumerate(sizes) if plan.devices[i] is Device.FAST) / tot if tot else 0.0

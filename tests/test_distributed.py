@@ -1,0 +1,119 @@
+"""ZeRO-3 partition + bucketed collectives: host-side logic on gloo, world 2."""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import paper_2410_21316_b200 as D
+from paper_2410_21316_b200.distributed import BucketedCollectives, ShardLayout, finalising_actions
+
+
+def _port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_layout_pads_ragged_last_rank():
+    lay = ShardLayout.build(1000, 3, 128)
+    assert lay.per_rank == 334 and lay.padded_total == 1002 and lay.num_buckets == 3
+    assert lay.bucket_span(2) == (256, 78)
+    assert lay.rank_of_bucket_piece(2, 2) == (76, 2)
+    assert lay.rank_of_bucket_piece(0, 2) == (78, 0)
+    lay = ShardLayout.build(70 * 10**9, 8, 10**8)
+    assert lay.num_buckets == 88 and lay.bucket_span(87) == (8_700_000_000, 50_000_000)
+
+
+def test_finalising_actions_cover_every_subgroup():
+    for stride in (1, 2, 3, D.ALL_CPU):
+        plan = D.build_plan(12, stride, static_ratio=0.25)
+        fin = finalising_actions(plan)
+        assert sorted(fin) == list(range(12))
+        for sg, aid in fin.items():
+            assert plan.actions[aid].lane.value != "cpu_compute"
+
+
+def _worker(rank, world, port, total, sg, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lay = ShardLayout.build(total, world, sg)
+        coll = BucketedCollectives(lay)
+        # every rank holds full-model grads = (rank + 1) * base
+        base = torch.arange(lay.padded_total, dtype=torch.float32)
+        full = base * (rank + 1)
+        mine = torch.zeros(lay.per_rank)
+        coll.reduce_scatter_all(full, mine)
+        want = base[rank * lay.per_rank:(rank + 1) * lay.per_rank] * sum(r + 1 for r in range(world))
+        ok_rs = torch.equal(mine, want)
+        # all-gather: each rank contributes rank-tagged params
+        shard_params = torch.full((lay.per_rank,), float(rank))
+        gathered = torch.full((lay.padded_total,), -1.0)
+        coll.all_gather_all(gathered, shard_params)
+        want_g = torch.cat([torch.full((lay.per_rank,), float(r)) for r in range(world)])
+        q.put((rank, ok_rs, torch.equal(gathered, want_g)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("total,sg", [(1000, 128), (4096, 512)])
+def test_bucketed_collectives_gloo_world2(total, sg):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, total, sg, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok_rs and ok_ag for _, ok_rs, ok_ag in res), res
+
+
+def _step_worker(rank, world, port, q):
+    """Per-rank host update of its shard equals the slice of a single-rank run."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import optistate_oracle as O
+
+        total, sg = 10_000, 1_000
+        full = O.initialize(total, sg, seed=3, lowp="bf16")
+        lay = ShardLayout.build(total, world, sg)
+        lo = rank * lay.per_rank
+        n = sum(g.size for g in lay.ranks[rank])
+        opt = D.ShardedOptimizer.allocate(n, sg, lowp="bf16")
+        for name, key in (("_p", "p"), ("_m", "m"), ("_v", "v"), ("_g", "g"), ("_w", "w")):
+            getattr(opt, name)[:] = full[key][lo:lo + n]
+        D.sequential_oracle(opt, D.AdamHyper())
+        w = torch.zeros(lay.per_rank, dtype=torch.int16)
+        w[:n] = torch.from_numpy(opt.model16.view(np.int16))
+        gathered = torch.zeros(lay.padded_total, dtype=torch.int16)
+        BucketedCollectives(lay).all_gather_all(gathered.view(torch.bfloat16), w.view(torch.bfloat16))
+        O.sequential_oracle(full)
+        q.put((rank, gathered[:total].numpy().view(np.uint16).tobytes() == full["w"].tobytes()))
+    except Exception as e:  # report instead of hanging the parent
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_update_then_gather_equals_single_rank():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_step_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res

@@ -146,3 +146,28 @@ def test_load_grads_from_device_tensor(h100):
     O.sequential_oracle(want)
     assert opt.params32.tobytes() == want["p"].tobytes() and res.model16.view(torch.int16).cpu().numpy().view(
         np.uint16).tobytes() == want["w"].tobytes()
+
+
+def test_host_io_mode_reads_host_grads_and_mirrors_working_copy(h100):
+    opt = D.ShardedOptimizer.initialize(90_000, 10_000, seed=12, lowp="bf16")
+    res = opt.to_device()
+    res.grads.zero_()  # device grads are stale: host_io must ship the host image
+    plan = D.build_plan(9, 2, static_ratio=0.25)
+    D.execute_plan(opt, plan, h100, HYPER, host_io=True)
+    assert "_w" not in res.host_stale  # mirrored inside the phase
+    want = O.sequential_oracle(O.initialize(90_000, 10_000, 12, "bf16"))
+    assert opt._w.tobytes() == want["w"].tobytes()
+    assert opt.params32.tobytes() == want["p"].tobytes()
+    assert res.model16.view(torch.int16).cpu().numpy().view(np.uint16).tobytes() == want["w"].tobytes()
+
+
+def test_b200_policy_refit_and_choice(h100):
+    from paper_2410_21316_b200 import policy
+
+    opt = D.ShardedOptimizer.initialize(400_000, 40_000, seed=1, lowp="bf16")
+    sizes = [g.size for g in opt.subgroups]
+    r = D.execute_plan(opt, D.build_plan(10, 2), h100, HYPER)
+    prof = policy.refit_profile(h100, r.measured, sizes)
+    assert prof.channel_params_per_s > 0 and prof.fast_update_params_per_s > 0
+    k, spans = policy.choose_stride(prof, sizes)
+    assert k in spans and spans[k] == min(spans.values())
