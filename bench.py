@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=25,
                     help="1e8-param subgroups timed for the cpu_baseline (~10 s on 16 cores)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--host-threads", type=int, default=0, help="H1 team size (0: all allowed cores / ranks)")
+    ap.add_argument("--static-variants", default="0.5,1.0",
+                    help="extra measured runs with HBM-resident static subgroups ('' to skip)")
     ap.add_argument("--profile-out", default=None)
     return ap.parse_args()
 
@@ -230,6 +233,8 @@ def main() -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    if args.host_threads > 0:
+        D._native.lib().dos_set_host_threads(args.host_threads)
     P = int(args.params)
     SG = int(args.subgroup)
     mine = D.shard(P, world, SG)[rank]
@@ -350,6 +355,57 @@ def main() -> None:
                "api": "execute_plan(..., host_io=True): grads from pinned host, working copy back to host",
                "host_resident_params": cpu_params * world}
 
+    # ---------------- iteration collectives (N > 1): bucketed NCCL reduce-scatter
+    # of bf16 grads before the phase and all-gather of the bf16 working copy after
+    collectives = None
+    if world > 1:
+        from paper_2410_21316_b200.distributed import BucketedCollectives, ShardLayout
+
+        lay = ShardLayout.build(P, world, SG)
+        coll = BucketedCollectives(lay)
+        tdt = torch.bfloat16 if args.lowp == "bf16" else torch.float16
+        full = torch.zeros(lay.padded_total, dtype=tdt, device=device)
+        mine_buf = torch.zeros(lay.per_rank, dtype=tdt, device=device)
+        coll.reduce_scatter_all(full, mine_buf)
+        coll.all_gather_all(full, mine_buf)
+        torch.cuda.synchronize()
+        c0, c1, c2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        barrier()
+        c0.record()
+        coll.reduce_scatter_all(full, mine_buf)
+        c1.record()
+        coll.all_gather_all(full, mine_buf)
+        c2.record()
+        torch.cuda.synchronize()
+        rs_ms, ag_ms = max_over_ranks(c0.elapsed_time(c1)), max_over_ranks(c1.elapsed_time(c2))
+        collectives = {"reduce_scatter_ms": rs_ms, "all_gather_ms": ag_ms, "buckets": lay.num_buckets,
+                       "bytes_per_rank_each": 2 * lay.padded_total,
+                       "iteration_update_ms": rs_ms + ms_max + ag_ms}
+        del full, mine_buf
+
+    # ---------------- static-resident variants: the same
+    # 7B phase with a fraction of subgroups' fp32 state resident in HBM
+    variants = []
+    for tok in [t for t in args.static_variants.split(",") if t.strip()]:
+        ratio = float(tok)
+        vstride, vspans = policy.choose_stride(profile, sizes, range(1, 7), ratio)
+        vplan = D.build_plan(nsg, vstride, static_ratio=ratio)
+        D.execute_plan(opt, vplan, profile, hyper)  # moves the residents into HBM (untimed)
+        barrier()
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        for _ in range(args.steps):
+            D.execute_plan(opt, vplan, profile, hyper)
+        g1.record()
+        torch.cuda.synchronize()
+        vms = max_over_ranks(g0.elapsed_time(g1) / args.steps)
+        variants.append({"static_ratio": ratio, "stride": vstride, "ms_per_step": vms, "value": P / (vms * 1e-3),
+                         "hbm_resident_state_bytes": 12 * sum(sizes[i] for i in vplan.static_set) * world})
+    if variants:
+        opt.residency.set_static(frozenset())  # back to pure offload
+        torch.cuda.empty_cache()
+
     # ---------------- CPU baseline: the oracle port on host cores (rank 0, N=1)
     cpu_baseline = None
     if rank == 0 and world == 1:
@@ -413,6 +469,8 @@ def main() -> None:
                         "host_contention": profile.host_contention,
                         "host_threads": D._native.lib().dos_host_threads()},
             "setup_s": {"alloc_pin": t_alloc, "fill": t_fill},
+            "static_variants": variants,
+            "collectives": collectives,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

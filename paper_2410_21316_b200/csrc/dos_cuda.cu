@@ -17,6 +17,8 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "dos_internal.h"
 #include "dos_numerics.h"
@@ -206,7 +208,209 @@ template <int GT, int LT>
 void launch_adam(float* p, float* m, float* v, const void* g, void* lp, int64_t head, int64_t nvec,
                  int64_t n, const dos_kscal& s, cudaStream_t st) {
   const int64_t work = nvec > 0 ? nvec : n;
-  k_adam<GT, LT><<<grid_for(work), kThreads, 0, st>>>(p, m, v, g, lp, head, nvec, n, s);
+  static int cap_blocks = 0;  // resident CTAs per SM for this instantiation
+  if (!cap_blocks) {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_adam<GT, LT>, kThreads, 0) != cudaSuccess || b < 1) b = 4;
+    cap_blocks = b;
+  }
+  const int64_t cap = (int64_t)sm_count() * cap_blocks;
+  int64_t want = (work + kThreads - 1) / kThreads;
+  want = want < 1 ? 1 : (want < cap ? want : cap);
+  k_adam<GT, LT><<<(unsigned)want, kThreads, 0, st>>>(p, m, v, g, lp, head, nvec, n, s);
+}
+
+// ---------------------------------------------------------------------------
+// K1, TMA-pipelined variant (the default for 16-bit grads).
+//
+// Persistent CTAs (one per SM) stream tiles of TE elements through an
+// S-stage shared-memory ring.  Thread 0 is the producer: for each tile it
+// arms the stage's mbarrier with the tile's byte count and issues four 1-D
+// bulk copies (cp.async.bulk, SASS UBLKCP) for p, m, v, g; S-1 tiles are
+// always in flight, decoupling HBM latency from the long IEEE div/sqrt
+// chains.  All threads then update the tile in place in shared memory (the
+// working copy overwrites the grads' slot), a proxy fence + barrier publish
+// the results, and thread 0 bulk-stores p, m, v and the working copy back
+// (cp.async.bulk.global.shared::cta, bulk_group).  A stage is refilled only
+// after cp.async.bulk.wait_group.read confirms its previous stores have
+// drained out of shared memory.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <int GT, int LT, int NT, int S>
+__global__ void __launch_bounds__(NT, 1)
+    k_adam_tma(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
+               const uint16_t* __restrict__ g, uint16_t* __restrict__ w, int64_t ntiles, dos_kscal s) {
+  constexpr int TE = 4 * NT;  // 4 elements per thread per tile
+  constexpr uint32_t F32B = TE * 4, H16B = TE * 2, STAGE = 3 * F32B + H16B;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full[S];
+  const int tid = threadIdx.x;
+  const int64_t first = blockIdx.x, step = gridDim.x;
+  const int64_t mine = ntiles > first ? (ntiles - first + step - 1) / step : 0;
+
+  auto stage_ptr = [&](int st, int piece) -> unsigned char* { return smem + st * STAGE + piece * F32B; };
+  auto issue = [&](int64_t k) {  // tile k of this CTA into stage k % S
+    const int st = (int)(k % S);
+    const int64_t e0 = (first + k * step) * TE;
+    mbar_expect_tx(&full[st], STAGE);
+    bulk_load(stage_ptr(st, 0), p + e0, F32B, &full[st]);
+    bulk_load(stage_ptr(st, 1), m + e0, F32B, &full[st]);
+    bulk_load(stage_ptr(st, 2), v + e0, F32B, &full[st]);
+    bulk_load(stage_ptr(st, 3), g + e0, H16B, &full[st]);
+  };
+
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
+    fence_async_smem();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int64_t k = 0; k < S - 1 && k < mine; ++k) issue(k);
+
+  for (int64_t k = 0; k < mine; ++k) {
+    const int st = (int)(k % S);
+    mbar_wait(&full[st], (uint32_t)((k / S) & 1));
+    float4* P = reinterpret_cast<float4*>(stage_ptr(st, 0)) + tid;
+    float4* M = reinterpret_cast<float4*>(stage_ptr(st, 1)) + tid;
+    float4* V = reinterpret_cast<float4*>(stage_ptr(st, 2)) + tid;
+    uint2* G = reinterpret_cast<uint2*>(stage_ptr(st, 3)) + tid;
+    float4 pp = *P, mm = *M, vv = *V;
+    const uint2 gg = *G;
+    float pe[4] = {pp.x, pp.y, pp.z, pp.w}, me[4] = {mm.x, mm.y, mm.z, mm.w}, ve[4] = {vv.x, vv.y, vv.z, vv.w};
+    const uint16_t gb[4] = {(uint16_t)(gg.x & 0xffffu), (uint16_t)(gg.x >> 16), (uint16_t)(gg.y & 0xffffu),
+                            (uint16_t)(gg.y >> 16)};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float gj = GT == DOS_BF16 ? dos_bf16_to_f32(gb[j]) : __half2float(__ushort_as_half(gb[j]));
+      dos_adam_elem(pe[j], me[j], ve[j], gj, s);
+    }
+    *P = make_float4(pe[0], pe[1], pe[2], pe[3]);
+    *M = make_float4(me[0], me[1], me[2], me[3]);
+    *V = make_float4(ve[0], ve[1], ve[2], ve[3]);
+    if (LT != DOS_NONE)
+      *G = make_uint2((uint32_t)to_lowp(pe[0], LT) | ((uint32_t)to_lowp(pe[1], LT) << 16),
+                      (uint32_t)to_lowp(pe[2], LT) | ((uint32_t)to_lowp(pe[3], LT) << 16));
+    fence_async_smem();  // generic-proxy smem writes -> visible to the bulk-copy (async) proxy
+    __syncthreads();
+    if (tid == 0) {
+      const int64_t e0 = (first + k * step) * TE;
+      bulk_store(p + e0, stage_ptr(st, 0), F32B);
+      bulk_store(m + e0, stage_ptr(st, 1), F32B);
+      bulk_store(v + e0, stage_ptr(st, 2), F32B);
+      if (LT != DOS_NONE) bulk_store(w + e0, stage_ptr(st, 3), H16B);
+      bulk_commit();
+      if (k + S - 1 < mine) {
+        bulk_wait_read<1>();  // the refilled stage's stores (tile k-1) have left shared memory
+        issue(k + S - 1);
+      }
+    }
+  }
+  if (tid == 0) bulk_wait_all();
+}
+
+template <int GT, int LT, int NT, int S>
+int launch_tma_cfg(float* p, float* m, float* v, const uint16_t* g, uint16_t* w, int64_t ntiles, const dos_kscal& s,
+                   int ctas_per_sm, cudaStream_t st) {
+  constexpr int smem = S * 4 * NT * 14;
+  static bool configured = false;
+  if (!configured) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(k_adam_tma<GT, LT, NT, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return dos_set_error(DOS_ECUDA, "K1 smem attribute: %s", cudaGetErrorString(e));
+    configured = true;
+  }
+  const int64_t cap = (int64_t)sm_count() * ctas_per_sm;
+  const int64_t grid = ntiles < cap ? ntiles : cap;
+  k_adam_tma<GT, LT, NT, S><<<(unsigned)grid, NT, smem, st>>>(p, m, v, g, w, ntiles, s);
+  return DOS_OK;
+}
+
+// Pipeline shapes (threads, stages, CTAs/SM); tile = 4 x threads elements,
+// 14 B/element of shared memory per stage.  DOS_K1_CFG=<index> selects one
+// for A/B sweeps; DOS_K1=ldg forces the register path.
+struct TmaCfg {
+  int nt, stages, cpb;
+};
+// Index 0 is the default: 1024 threads, 3 x 56 KB stages, one CTA per SM
+// (swept on the B200: profiles/k1_pipeline_sweep.json).
+constexpr TmaCfg kTmaCfgs[] = {{1024, 3, 1}, {512, 6, 1}, {256, 12, 1}, {256, 6, 2}, {512, 3, 2},
+                               {128, 12, 2}, {1024, 4, 1}, {1024, 2, 2}, {512, 4, 2}};
+
+const TmaCfg& tma_cfg() {
+  static int idx = -1;
+  if (idx < 0) {
+    const char* e = getenv("DOS_K1_CFG");
+    idx = e ? atoi(e) : 0;
+    if (idx < 0 || idx >= (int)(sizeof(kTmaCfgs) / sizeof(kTmaCfgs[0]))) idx = 0;
+  }
+  return kTmaCfgs[idx];
+}
+
+bool tma_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("DOS_K1");
+    on = (e && strcmp(e, "ldg") == 0) ? 0 : 1;
+  }
+  return on == 1;
+}
+
+template <int GT, int LT>
+int launch_adam_tma(float* p, float* m, float* v, const uint16_t* g, uint16_t* w, int64_t ntiles, const dos_kscal& s,
+                    cudaStream_t st) {
+  const TmaCfg& c = tma_cfg();
+#define DOS_CFG(NT_, S_) \
+  if (c.nt == NT_ && c.stages == S_) return launch_tma_cfg<GT, LT, NT_, S_>(p, m, v, g, w, ntiles, s, c.cpb, st);
+  DOS_CFG(1024, 3)
+  DOS_CFG(512, 6)
+  DOS_CFG(256, 12)
+  DOS_CFG(256, 6)
+  DOS_CFG(512, 3)
+  DOS_CFG(128, 12)
+  DOS_CFG(1024, 4)
+  DOS_CFG(1024, 2)
+  DOS_CFG(512, 4)
+#undef DOS_CFG
+  return dos_set_error(DOS_EINVAL, "no K1 pipeline shape %d/%d", c.nt, c.stages);
 }
 
 }  // namespace
@@ -234,6 +438,32 @@ int dos_adam_launch(float* p, float* m, float* v, const void* g, int gt, void* l
   const void* ptrs[5] = {p, m, v, g, lp};
   const int eb[5] = {4, 4, 4, gt == DOS_F32 ? 4 : 2, 2};
   int64_t head = common_head(ptrs, eb, lt == DOS_NONE ? 4 : 5, n);
+  // TMA path: 16-bit grads, a 16-byte-alignable range of at least one tile.
+  if (gt != DOS_F32 && (lt == DOS_NONE || lt == DOS_F16 || lt == DOS_BF16) && head >= 0 && tma_enabled() &&
+      (n - head) / (4 * tma_cfg().nt) >= 1) {
+    const int64_t tile = 4 * tma_cfg().nt;
+    const int64_t ntiles = (n - head) / tile;
+    const int64_t body_end = head + ntiles * tile;
+    const char* gc = static_cast<const char*>(g);
+    char* lc = static_cast<char*>(lp);
+    int rc = DOS_OK;
+    if (head > 0) rc = dos_adam_launch(p, m, v, g, gt, lp, lt, head, s, st);  // < 8 elements: register path
+    if (rc != DOS_OK) return rc;
+    const uint16_t* gb = reinterpret_cast<const uint16_t*>(gc + 2 * head);
+    uint16_t* wb = lt == DOS_NONE ? nullptr : reinterpret_cast<uint16_t*>(lc + 2 * head);
+#define DOS_TMA(G, L) \
+  if (gt == G && lt == L) rc = launch_adam_tma<G, L>(p + head, m + head, v + head, gb, wb, ntiles, s, st);
+    DOS_TMA(DOS_F16, DOS_NONE) else DOS_TMA(DOS_F16, DOS_F16) else DOS_TMA(DOS_F16, DOS_BF16)
+    else DOS_TMA(DOS_BF16, DOS_NONE) else DOS_TMA(DOS_BF16, DOS_F16) else DOS_TMA(DOS_BF16, DOS_BF16)
+#undef DOS_TMA
+    if (rc != DOS_OK) return rc;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return dos_set_error(DOS_ECUDA, "K1 (TMA) launch failed: %s", cudaGetErrorString(e));
+    if (body_end < n)
+      rc = dos_adam_launch(p + body_end, m + body_end, v + body_end, gc + 2 * body_end, gt,
+                           lt == DOS_NONE ? nullptr : static_cast<void*>(lc + 2 * body_end), lt, n - body_end, s, st);
+    return rc;
+  }
   int64_t nvec = 0;
   if (head < 0) {
     head = n;  // no common alignment: everything takes the scalar path
