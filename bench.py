@@ -57,6 +57,7 @@ def parse():
                     help="1e8-param subgroups timed for the cpu_baseline (~10 s on 16 cores)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--host-threads", type=int, default=0, help="H1 team size (0: all allowed cores / ranks)")
+    ap.add_argument("--trace-dir", default=None, help="write measured/predicted timelines as trace CSVs")
     ap.add_argument("--static-variants", default="0.5,1.0",
                     help="extra measured runs with HBM-resident static subgroups ('' to skip)")
     ap.add_argument("--profile-out", default=None)
@@ -414,6 +415,16 @@ def main() -> None:
         cpu_baseline = {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "port",
                         "sample": f"{args.cpu_sample} x {SG:.0e}-param subgroups ({r['seconds']:.1f} s), "
                                   f"oracle/adam_oracle.c with {threads} threads"}
+
+    if rank == 0 and args.trace_dir:
+        from paper_2410_21316_b200.timing import write_trace_csv
+
+        os.makedirs(args.trace_dir, exist_ok=True)
+        tag = f"{P / 1e9:g}B_stride{stride}"
+        with open(os.path.join(args.trace_dir, f"measured_{tag}.csv"), "w") as fh:
+            write_trace_csv(results[-1].measured, fh)
+        with open(os.path.join(args.trace_dir, f"predicted_{tag}.csv"), "w") as fh:
+            write_trace_csv(results[-1].timeline, fh)
 
     if rank == 0:
         line = {

@@ -158,6 +158,21 @@ def memory_trace(events: Iterable[ScheduledAction], plan: UpdatePlan,
     return trace
 
 
+TRACE_HEADER = ("event_id", "lane", "kind", "subgroup", "start_ns", "end_ns", "bytes")
+
+
+def write_trace_csv(timeline: Timeline, stream) -> None:
+    """Timeline as CSV in the reference's trace schema (cli.py:49,250-264);
+    works for predicted and measured timelines alike."""
+    import csv
+
+    w = csv.writer(stream)
+    w.writerow(TRACE_HEADER)
+    for ev in timeline.events:
+        a = ev.action
+        w.writerow((a.id, a.lane.value, a.kind.value, a.subgroup, ev.start_ns, ev.end_ns, ev.bytes))
+
+
 class GradFlushStrategy(str, enum.Enum):
     """How half-precision grads reach the host as fp32 (sim.py:226-243)."""
 
