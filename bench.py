@@ -50,7 +50,9 @@ def parse():
     ap.add_argument("--subgroup", type=float, default=1e8)
     ap.add_argument("--lowp", default="bf16", choices=["bf16", "fp16"])
     ap.add_argument("--stride", default="auto")
-    ap.add_argument("--static-ratio", type=float, default=0.0)
+    ap.add_argument("--static-ratio", type=float, default=0.2,
+                    help="fraction of subgroups whose fp32 state stays in HBM (TwinFlow-style residents); 0.2 is "
+                         "the paper's representative setting (PAPER.md:631-635); the rest is host-offloaded")
     ap.add_argument("--capacity-gb", type=float, default=None,
                     help="imposed dynamic fast-tier budget (default: two windows)")
     ap.add_argument("--cpu-sample", type=int, default=25,
@@ -58,7 +60,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--host-threads", type=int, default=0, help="H1 team size (0: all allowed cores / ranks)")
     ap.add_argument("--trace-dir", default=None, help="write measured/predicted timelines as trace CSVs")
-    ap.add_argument("--static-variants", default="0.5,1.0",
+    ap.add_argument("--static-variants", default="0.0,0.5,1.0",
                     help="extra measured runs with HBM-resident static subgroups ('' to skip)")
     ap.add_argument("--profile-out", default=None)
     return ap.parse_args()
@@ -265,12 +267,24 @@ def main() -> None:
     else:
         stride = int(args.stride)
     plan = D.build_plan(nsg, stride, static_ratio=args.static_ratio)
-    for w in range(args.warmup):
+    tuned = None
+    if args.stride == "auto":
+        # calibration (untimed, before the warm-up): one step on the reference
+        # planner's plan, re-fit the constants from its measured timeline, then
+        # explore the model's best candidates by measurement (StrideTuner).
         r = D.execute_plan(opt, plan, profile, hyper)
-        if w == 0 and args.stride == "auto":
-            profile = policy.refit_profile(profile, r.measured, sizes)
-            stride, stride_spans = policy.choose_stride(profile, sizes, range(1, 7), args.static_ratio)
-            plan = D.build_plan(nsg, stride, static_ratio=args.static_ratio)
+        profile = policy.refit_profile(profile, r.measured, sizes)
+        tuner = policy.StrideTuner(profile, sizes, range(1, 7), args.static_ratio, explore=4)
+        stride_spans = tuner.predicted
+        while tuner.exploring:
+            k = tuner.next_stride()
+            r = D.execute_plan(opt, D.build_plan(nsg, k, static_ratio=args.static_ratio), profile, hyper)
+            tuner.record(k, max_over_ranks(r.measured.span_ns))
+        stride = tuner.next_stride()
+        plan = tuner.plan()
+        tuned = {str(k): v / 1e6 for k, v in sorted(tuner.measured.items())}
+    for w in range(args.warmup):
+        D.execute_plan(opt, plan, profile, hyper)
     torch.cuda.synchronize()
 
     # ---------------- timed region: device-resident grads (value)
@@ -280,6 +294,7 @@ def main() -> None:
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     results = []
+    launches0 = D._native.lib().dos_launch_count()
     torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include timed/ captures exactly this region
     e0.record()
     for _ in range(args.steps):
@@ -296,6 +311,7 @@ def main() -> None:
     # per-step measured phase, K1 roofline from the measured GPU_UPDATE events
     spans = [r.measured.span_ns for r in results]
     makespans = [r.measured.makespan_ns for r in results]
+    gpu_launches = D._native.lib().dos_launch_count() - launches0  # libdos kernels in the timed region
     k1_ns, k1_params, k1_launches = 0, 0, 0
     h2d_b = d2h_b = 0
     lane_busy = {}
@@ -389,9 +405,13 @@ def main() -> None:
     variants = []
     for tok in [t for t in args.static_variants.split(",") if t.strip()]:
         ratio = float(tok)
-        vstride, vspans = policy.choose_stride(profile, sizes, range(1, 7), ratio)
-        vplan = D.build_plan(nsg, vstride, static_ratio=ratio)
-        D.execute_plan(opt, vplan, profile, hyper)  # moves the residents into HBM (untimed)
+        vt = policy.StrideTuner(profile, sizes, range(1, 7), ratio, explore=3)
+        while vt.exploring:  # untimed; the first step also moves the residents into HBM
+            k = vt.next_stride()
+            r = D.execute_plan(opt, D.build_plan(nsg, k, static_ratio=ratio), profile, hyper)
+            vt.record(k, max_over_ranks(r.measured.span_ns))
+        vstride, vplan = vt.next_stride(), vt.plan()
+        D.execute_plan(opt, vplan, profile, hyper)
         barrier()
         torch.cuda.synchronize()
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -404,7 +424,7 @@ def main() -> None:
         variants.append({"static_ratio": ratio, "stride": vstride, "ms_per_step": vms, "value": P / (vms * 1e-3),
                          "hbm_resident_state_bytes": 12 * sum(sizes[i] for i in vplan.static_set) * world})
     if variants:
-        opt.residency.set_static(frozenset())  # back to pure offload
+        opt.residency.set_static(plan.static_set)  # back to the headline placement
         torch.cuda.empty_cache()
 
     # ---------------- CPU baseline: the oracle port on host cores (rank 0, N=1)
@@ -442,13 +462,15 @@ def main() -> None:
             "data": "synthetic (seeded, generated on device)",
             "config": {
                 "workload": f"{P / 1e9:g}B-param fp32 Adam shard, {args.lowp} grads + working copy, "
-                            f"host offload (BASELINE configs[1])",
+                            f"host offload of {100 * (1 - args.static_ratio):g}% of the optimizer state "
+                            f"({100 * args.static_ratio:g}% HBM-resident, TwinFlow-style) (BASELINE configs[1])",
                 "params": P, "subgroup": SG, "subgroups_per_rank": nsg, "lowp": args.lowp,
                 "stride": "all_cpu" if stride is D.ALL_CPU else stride,
                 "planner_k": "all_cpu" if planner_stride is D.ALL_CPU else planner_stride,
                 "k_real": choice.k_real,
                 "predicted_span_ms_by_stride": None if stride_spans is None else
                 {str(k): v / 1e6 for k, v in stride_spans.items()},
+                "measured_span_ms_by_stride": tuned,
                 "static_ratio": args.static_ratio, "fast_capacity_bytes": cap, "hbm_windows": results[0].measured and
                 min(2, 2 if cap is None else cap // (12 * SG)),
                 "parallelism": f"zero3-shard{world}", "l2": "inputs > L2 (28 B/param over 1e8-param subgroups)",
@@ -472,7 +494,8 @@ def main() -> None:
             },
             "cpu_baseline": cpu_baseline,
             "e2e": e2e,
-            "gpu_launches": k1_launches,
+            "gpu_launches": gpu_launches,
+            "k1_updates": k1_launches,
             "clocks": clk,
             "profile": {"channel_params_per_s": profile.channel_params_per_s,
                         "fast_update_params_per_s": profile.fast_update_params_per_s,

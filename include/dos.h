@@ -61,6 +61,8 @@ typedef struct dos_adam_scalars {
 
 const char* dos_last_error(void);
 int dos_version(void);
+/* Number of libdos kernels launched by this process so far (K1 + conversions). */
+int64_t dos_launch_count(void);
 
 /* ---- K1: fused Adam on the GPU (sm_100a).  Asynchronous on `stream`
  * (a cudaStream_t; NULL = legacy default).  p/m/v fp32 in place; g in

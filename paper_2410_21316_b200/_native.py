@@ -78,6 +78,7 @@ _VP, _I, _I64, _SZ = C.c_void_p, C.c_int, C.c_int64, C.c_size_t
 SIGNATURES: dict[str, tuple] = {
     "dos_last_error": (C.c_char_p, []),
     "dos_version": (_I, []),
+    "dos_launch_count": (_I64, []),
     "dos_adam_step_cuda": (_I, [_VP, _VP, _VP, _VP, _I, _VP, _I, _I64, C.POINTER(dos_adam_scalars), _VP]),
     "dos_adam_step_host": (_I, [_VP, _VP, _VP, _VP, _I, _VP, _I, _I64, C.POINTER(dos_adam_scalars), _I]),
     "dos_downscale_host": (_I, [_VP, _VP, _I, _I64, _I]),

@@ -20,10 +20,14 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <atomic>
+
 #include "dos_internal.h"
 #include "dos_numerics.h"
 
 namespace {
+
+std::atomic<int64_t> g_launches{0};  // every libdos kernel launch (dos_launch_count)
 
 constexpr int kThreads = 256;
 constexpr int kVec = 8;  // elements per thread per trip
@@ -218,6 +222,7 @@ void launch_adam(float* p, float* m, float* v, const void* g, void* lp, int64_t 
   int64_t want = (work + kThreads - 1) / kThreads;
   want = want < 1 ? 1 : (want < cap ? want : cap);
   k_adam<GT, LT><<<(unsigned)want, kThreads, 0, st>>>(p, m, v, g, lp, head, nvec, n, s);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 // ---------------------------------------------------------------------------
@@ -361,6 +366,7 @@ int launch_tma_cfg(float* p, float* m, float* v, const uint16_t* g, uint16_t* w,
   const int64_t cap = (int64_t)sm_count() * ctas_per_sm;
   const int64_t grid = ntiles < cap ? ntiles : cap;
   k_adam_tma<GT, LT, NT, S><<<(unsigned)grid, NT, smem, st>>>(p, m, v, g, w, ntiles, s);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   return DOS_OK;
 }
 
@@ -511,6 +517,7 @@ extern "C" int dos_downscale_cuda(const float* x, void* out, int out_dtype, int6
     k_down<DOS_F16><<<grid, kThreads, 0, st>>>(x, reinterpret_cast<uint16_t*>(out), head, nvec, n);
   else
     k_down<DOS_BF16><<<grid, kThreads, 0, st>>>(x, reinterpret_cast<uint16_t*>(out), head, nvec, n);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return dos_set_error(DOS_ECUDA, "downscale launch failed: %s", cudaGetErrorString(e));
   return DOS_OK;
@@ -531,7 +538,10 @@ extern "C" int dos_upscale_cuda(const void* x, int in_dtype, float* out, int64_t
     k_up<DOS_F16><<<grid, kThreads, 0, st>>>(reinterpret_cast<const uint16_t*>(x), out, head, nvec, n);
   else
     k_up<DOS_BF16><<<grid, kThreads, 0, st>>>(reinterpret_cast<const uint16_t*>(x), out, head, nvec, n);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return dos_set_error(DOS_ECUDA, "upscale launch failed: %s", cudaGetErrorString(e));
   return DOS_OK;
 }
+
+extern "C" int64_t dos_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
