@@ -1,6 +1,9 @@
 // dos_host_isa.cpp — one ISA build of the H1 loops; compiled three times
 // (-DDOS_ISA_NS=avx512 -mavx512f..., avx2, generic) and picked at run time.
 #include "dos_internal.h"
+#if defined(__AVX512F__)
+#include <immintrin.h>
+#endif
 
 #ifndef DOS_ISA_NS
 #error "DOS_ISA_NS must name the ISA variant"

@@ -300,3 +300,46 @@ def test_sweep_orders_v100(v100):
     spans = [e.makespan_ns for e in res.entries]
     assert spans == sorted(spans) and len(set(spans)) == 4
     assert res.best_k == 2
+
+
+# ------------------------------------------------------------------ B200 policy
+
+
+def test_b200_model_timelines_validate_without_stream_fifo(h100):
+    from paper_2410_21316_b200 import policy
+
+    for stride in (1, 2, 3, 4):
+        for ratio in (0.0, 0.25):
+            plan = build_plan(12, stride, ratio)
+            tl = policy.simulate_b200_phase(plan, h100, 10**8)
+            t = D.SimTarget(h100, plan, 10**8)
+            D.validate_schedule(plan, tl.events, t, check_streams=False, max_windows=2)
+            # relaxing the one-buffer-per-stream rule never makes the phase slower
+            assert tl.span_ns <= D.simulate_update_phase(plan, h100, 10**8).span_ns
+
+
+def test_stride_tuner_explores_then_exploits(h100):
+    from paper_2410_21316_b200 import policy
+
+    tuner = policy.StrideTuner(h100, [10**8] * 20, range(1, 7), explore=3)
+    tried = []
+    fake = {1: 900, 2: 500, 3: 400, 4: 450, 5: 700, 6: 800}
+    while tuner.exploring:
+        k = tuner.next_stride()
+        tried.append(k)
+        tuner.record(k, fake[k])
+    assert len(tried) == 3 and len(set(tried)) == 3
+    assert tuner.next_stride() == min(tried, key=fake.get)
+    assert tuner.plan().stride == tuner.next_stride()
+
+
+def test_refit_profile_from_a_timeline(h100):
+    from paper_2410_21316_b200 import policy
+
+    plan = build_plan(8, 2)
+    tl = D.simulate_update_phase(plan, h100, 10**8)
+    prof = policy.refit_profile(h100, tl, [10**8] * 8)
+    # a timeline produced from the profile's own rates re-fits to (nearly) those rates
+    assert prof.channel_params_per_s == pytest.approx(h100.channel_params_per_s, rel=1e-6)
+    assert prof.fast_update_params_per_s == pytest.approx(h100.fast_update_params_per_s, rel=1e-6)
+    assert prof.cpu_update_params_per_s == pytest.approx(h100.cpu_update_params_per_s, rel=1e-6)

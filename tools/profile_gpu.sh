@@ -7,7 +7,7 @@ mkdir -p gpurun_out
 ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches.csv \
     python bench.py --params 2e9 --steps 1 --warmup 2 --no-e2e --cpu-sample 1 > gpurun_out/launches_bench.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_adam -s 3 -c 1 -f -o gpurun_out/k1_full \
+ncu --set full --clock-control none --import-source on -k regex:k_adam_tma -s 3 -c 1 -f -o gpurun_out/k1_full \
     python tools/k1_once.py > gpurun_out/k1_full.log 2>&1
 ncu -i gpurun_out/k1_full.ncu-rep --page raw --csv > gpurun_out/k1_full_raw.csv 2>/dev/null
 ncu -i gpurun_out/k1_full.ncu-rep --page source --csv > gpurun_out/k1_full_source.csv 2>/dev/null

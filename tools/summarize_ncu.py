@@ -16,7 +16,10 @@ def launches(path):
             continue
         name = r["Kernel Name"]
         if "k_adam" in name or "k_down" in name or "k_up" in name:
-            short = "libdos:" + name.split("<")[0].split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "")
+            import re
+
+            mt = re.search(r"(k_[a-z_]+)(<[^>]*>)?", name)
+            short = "libdos:" + (mt.group(1) + (mt.group(2) or "") if mt else name[:60])
         else:
             short = "torch:" + name.split("(")[0][-70:]
         tot[short][0] += 1
