@@ -171,6 +171,11 @@ int dos_exec_submit(void* ex, const dos_action_desc* a);
 /* Wait for the phase; fills measured [start,end) in ns since t0 per action id
  * (arrays of length >= number of submitted actions). */
 int dos_exec_finish(void* ex, int64_t* start_ns, int64_t* end_ns, int32_t n);
+/* Make `stream` (a cudaStream_t) wait until submitted device action `id` of
+ * the current phase has finished — e.g. start the all-gather of a subgroup's
+ * working copy as soon as its GPU_UPDATE / H2D_PARAMS16 is done, while the
+ * rest of the phase still runs.  Host-lane actions are rejected (EINVAL). */
+int dos_exec_stream_wait(void* ex, int32_t id, void* stream);
 /* Device pointer of a staging slot piece (0=m,1=v,2=p) for tests/inspection. */
 int dos_exec_slot_ptr(void* ex, int32_t slot, int32_t piece, float** out);
 

@@ -95,6 +95,7 @@ SIGNATURES: dict[str, tuple] = {
     "dos_exec_submit": (_I, [_VP, C.POINTER(dos_action_desc)]),
     "dos_exec_finish": (_I, [_VP, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_int32]),
     "dos_exec_slot_ptr": (_I, [_VP, C.c_int32, C.c_int32, C.POINTER(C.POINTER(C.c_float))]),
+    "dos_exec_stream_wait": (_I, [_VP, C.c_int32, _VP]),
 }
 
 _lock = threading.Lock()

@@ -537,6 +537,17 @@ extern "C" int dos_exec_finish(void* ex, int64_t* start_ns, int64_t* end_ns, int
   return static_cast<Engine*>(ex)->finish(start_ns, end_ns, n);
 }
 
+extern "C" int dos_exec_stream_wait(void* ex, int32_t id, void* stream) {
+  if (!ex) return dos_set_error(DOS_EINVAL, "NULL engine");
+  Engine* e = static_cast<Engine*>(ex);
+  if (!e->active) return dos_set_error(DOS_ESTATE, "no active phase");
+  if (id < 0 || id >= e->count) return dos_set_error(DOS_EINVAL, "action %d was not submitted", id);
+  if (e->is_host[id]) return dos_set_error(DOS_EINVAL, "action %d runs on the host lane (no device event)", id);
+  const cudaError_t r = cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), e->ev_e[id], 0);
+  if (r != cudaSuccess) return dos_set_error(DOS_ECUDA, "cudaStreamWaitEvent: %s", cudaGetErrorString(r));
+  return DOS_OK;
+}
+
 extern "C" int dos_exec_slot_ptr(void* ex, int32_t slot, int32_t piece, float** out) {
   if (!ex || !out) return dos_set_error(DOS_EINVAL, "NULL engine or out");
   Engine* e = static_cast<Engine*>(ex);

@@ -322,6 +322,11 @@ class B200Target(SimTarget):
                    N.DOS_EINVAL: ValueError, N.DOS_ETYPE: TypeError}.get(rc, RuntimeError)
             raise exc(f"submit of action {action.id}: {msg}")
 
+    def stream_wait(self, action_id: int, stream) -> None:
+        """Make a torch/CUDA ``stream`` wait for submitted device action ``action_id``."""
+        handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+        N.check(N.lib().dos_exec_stream_wait(self.engine.handle, int(action_id), handle))
+
     def finish(self, raise_errors: bool = True) -> tuple[ScheduledAction, ...]:
         """Wait for the phase; measured events in emission order."""
         if not self._begun:

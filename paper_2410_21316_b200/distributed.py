@@ -139,6 +139,45 @@ class BucketedCollectives:
                 w.wait()
 
 
+def gather_params_overlapped(coll: BucketedCollectives, plan, working_copy, full_params, comm_stream=None):
+    """``execute_plan(..., on_submitted=...)`` hook: all-gather each bucket as
+    soon as this rank's subgroup j has its final working copy.
+
+    ``working_copy`` is this rank's device working copy (``residency.model16``),
+    ``full_params`` the padded full-model buffer.  Returns a callable taking the
+    B200Target; after it runs, every bucket's all-gather is queued on NCCL
+    behind the engine event of the action that finalised that subgroup, so the
+    gathers overlap the rest of the phase.
+    """
+    import torch
+
+    fin = finalising_actions(plan)
+    lay = coll.layout
+    rank = coll.rank
+
+    def hook(target) -> list:
+        stream = comm_stream or torch.cuda.Stream(device=working_copy.device)
+        works = []
+        with torch.cuda.stream(stream):
+            for j in range(lay.num_buckets):
+                start, size = lay.bucket_span(j)
+                valid, pad = lay.rank_of_bucket_piece(rank, j)
+                if valid:
+                    target.stream_wait(fin[j], stream)
+                if pad:
+                    piece = torch.zeros(size, dtype=working_copy.dtype, device=working_copy.device)
+                    if valid:
+                        piece[:valid].copy_(working_copy[start:start + valid])
+                else:
+                    piece = working_copy[start:start + size]
+                works.append(coll.all_gather_bucket(full_params, piece, j))
+        hook.works = works
+        hook.stream = stream
+        return works
+
+    return hook
+
+
 def finalising_actions(plan) -> dict[int, int]:
     """Subgroup -> id of the device action after which its working copy is final.
 

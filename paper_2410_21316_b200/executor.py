@@ -171,6 +171,7 @@ def execute_plan(
     host_io: bool = False,
     check_coherence: bool = False,
     validate_measured: bool = True,
+    on_submitted=None,
 ) -> ExecutionResult:
     """Run one optimizer step of ``plan`` on the B200; mutates ``optimizer``.
 
@@ -194,6 +195,8 @@ def execute_plan(
     target = B200Target(profile, plan, optimizer, hyper, step, host_threads=host_threads, host_io=host_io)
     try:
         events = run_update(plan, target)
+        if on_submitted is not None:  # e.g. chain per-subgroup collectives onto engine events
+            on_submitted(target)
     except BaseException:
         target.finish(raise_errors=False)
         raise
