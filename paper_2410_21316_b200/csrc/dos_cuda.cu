@@ -305,6 +305,7 @@ __global__ void __launch_bounds__(NT, 1)
 
   if (tid == 0) {
     for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");  // inits visible to the async proxy
     fence_async_smem();
   }
   __syncthreads();
