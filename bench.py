@@ -242,6 +242,15 @@ def main() -> None:
     SG = int(args.subgroup)
     mine = D.shard(P, world, SG)[rank]
     P_rank = sum(g.size for g in mine)
+    # CPU baseline first (rank 0, N=1): the oracle port on the host cores,
+    # measured before the 112 GB pinned shard exists, like the reference arm.
+    cpu_baseline = None
+    if rank == 0 and world == 1:
+        threads = len(os.sched_getaffinity(0))
+        r = cpu_oracle_rate(int(args.subgroup), args.cpu_sample, args.lowp, threads)
+        cpu_baseline = {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "port",
+                        "sample": f"{args.cpu_sample} x {args.subgroup:.0e}-param subgroups ({r['seconds']:.1f} s), "
+                                  f"oracle/adam_oracle.c (reference loop restated) with {threads} threads"}
     t_setup = time.perf_counter()
     opt = D.ShardedOptimizer.allocate(P_rank, SG, lowp=args.lowp)
     t_alloc = time.perf_counter() - t_setup
@@ -274,7 +283,15 @@ def main() -> None:
         # explore the model's best candidates by measurement (StrideTuner).
         r = D.execute_plan(opt, plan, profile, hyper)
         profile = policy.refit_profile(profile, r.measured, sizes)
+        if world > 1:  # every rank must explore the same candidates in the same order
+            box = [profile]
+            dist.broadcast_object_list(box, src=0)
+            profile = box[0]
         tuner = policy.StrideTuner(profile, sizes, range(1, 7), args.static_ratio, explore=4)
+        if world > 1:
+            box = [tuner.queue]
+            dist.broadcast_object_list(box, src=0)
+            tuner.queue = list(box[0])
         stride_spans = tuner.predicted
         while tuner.exploring:
             k = tuner.next_stride()
@@ -421,6 +438,10 @@ def main() -> None:
     for tok in [t for t in args.static_variants.split(",") if t.strip()]:
         ratio = float(tok)
         vt = policy.StrideTuner(profile, sizes, range(1, 7), ratio, explore=3)
+        if world > 1:
+            box = [vt.queue]
+            dist.broadcast_object_list(box, src=0)
+            vt.queue = list(box[0])
         while vt.exploring:  # untimed; the first step also moves the residents into HBM
             k = vt.next_stride()
             r = D.execute_plan(opt, D.build_plan(nsg, k, static_ratio=ratio), profile, hyper)
@@ -441,15 +462,6 @@ def main() -> None:
     if variants:
         opt.residency.set_static(plan.static_set)  # back to the headline placement
         torch.cuda.empty_cache()
-
-    # ---------------- CPU baseline: the oracle port on host cores (rank 0, N=1)
-    cpu_baseline = None
-    if rank == 0 and world == 1:
-        threads = len(os.sched_getaffinity(0))
-        r = cpu_oracle_rate(SG, args.cpu_sample, args.lowp, threads)
-        cpu_baseline = {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "port",
-                        "sample": f"{args.cpu_sample} x {SG:.0e}-param subgroups ({r['seconds']:.1f} s), "
-                                  f"oracle/adam_oracle.c with {threads} threads"}
 
     if rank == 0 and args.trace_dir:
         from paper_2410_21316_b200.timing import write_trace_csv
