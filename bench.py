@@ -361,7 +361,18 @@ def main() -> None:
     t_hbm = BYTES_PER_PARAM_K1 * fast_params / (hbm_peak * 1e9)
     t_link = max(h2d_b, d2h_b) / link_Bps
     t_host = (P_rank - fast_params) / profile.cpu_update_params_per_s
-    phase_ideal = max(t_hbm, t_link)
+    # host DRAM: every streamed param costs 24 B of DMA (12 read + 12 written),
+    # every host-updated param 28 B of H1 traffic + 2 B read by its H2D_PARAMS16;
+    # rate = measured H1 + duplex DMA sharing the host memory (profile_b200)
+    static_params = sum(opt.subgroups[i].size for i in plan.static_set)
+    dyn_fast = fast_params - static_params
+    cpu_params = P_rank - fast_params
+    host_bytes = 24 * dyn_fast + 30 * cpu_params
+    dram_Bps = profile_b200.LAST_RAW.get("h1_with_dma", {}).get("host_dram_GBs_combined", 0.0) * 1e9
+    t_dram = host_bytes / dram_Bps if dram_Bps else 0.0
+    bounds = {"hbm": t_hbm, "link": t_link, "host_dram": t_dram}
+    phase_bound = max(bounds, key=bounds.get)
+    phase_ideal = bounds[phase_bound]
 
     # ---------------- e2e through the public API with host buffers
     e2e = None
@@ -515,9 +526,13 @@ def main() -> None:
                          "kernel": "K1 dos_adam (fused Adam + bf16 copy)",
                          "bytes_per_param": BYTES_PER_PARAM_K1, "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
             "phase_roofline": {
-                "bound": "link" if t_link >= t_hbm else "hbm",
+                "bound": phase_bound,
                 "ideal_ms": phase_ideal * 1e3, "achieved_ms": ms_max, "frac": phase_ideal * 1e3 / ms_max,
-                "link_GBs_per_dir_measured": link_Bps / 1e9, "host_update_ms_at_measured_rate": t_host * 1e3,
+                "bounds_ms": {k: v * 1e3 for k, v in bounds.items()},
+                "link_GBs_per_dir_measured": link_Bps / 1e9,
+                "host_dram_bytes_per_step": host_bytes,
+                "host_dram_GBs_measured": dram_Bps / 1e9,
+                "host_update_ms_at_measured_rate": t_host * 1e3,
             },
             "cpu_baseline": cpu_baseline,
             "e2e": e2e,

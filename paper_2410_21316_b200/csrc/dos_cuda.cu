@@ -283,7 +283,8 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 template <int GT, int LT, int NT, int S>
 __global__ void __launch_bounds__(NT, 1)
     k_adam_tma(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
-               const uint16_t* __restrict__ g, uint16_t* __restrict__ w, int64_t ntiles, dos_kscal s) {
+               const uint16_t* __restrict__ g, uint16_t* __restrict__ w, int64_t ntiles, int64_t tail,
+               dos_kscal s) {
   constexpr int TE = 4 * NT;  // 4 elements per thread per tile
   constexpr uint32_t F32B = TE * 4, H16B = TE * 2, STAGE = 3 * F32B + H16B;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -350,12 +351,27 @@ __global__ void __launch_bounds__(NT, 1)
       }
     }
   }
+  // the ragged tail (< one tile) after the last tile: the last CTA, straight
+  // from global memory, so a subgroup is one launch
+  if (blockIdx.x == gridDim.x - 1) {
+    const int64_t base = ntiles * TE;
+    for (int64_t j = tid; j < tail; j += NT) {
+      const int64_t e = base + j;
+      float pe = p[e], me = m[e], ve = v[e];
+      const float gj = GT == DOS_BF16 ? dos_bf16_to_f32(g[e]) : __half2float(__ushort_as_half(g[e]));
+      dos_adam_elem(pe, me, ve, gj, s);
+      p[e] = pe;
+      m[e] = me;
+      v[e] = ve;
+      if (LT != DOS_NONE) w[e] = to_lowp(pe, LT);
+    }
+  }
   if (tid == 0) bulk_wait_all();
 }
 
 template <int GT, int LT, int NT, int S>
-int launch_tma_cfg(float* p, float* m, float* v, const uint16_t* g, uint16_t* w, int64_t ntiles, const dos_kscal& s,
-                   int ctas_per_sm, cudaStream_t st) {
+int launch_tma_cfg(float* p, float* m, float* v, const uint16_t* g, uint16_t* w, int64_t ntiles, int64_t tail,
+                   const dos_kscal& s, int ctas_per_sm, cudaStream_t st) {
   constexpr int smem = S * 4 * NT * 14;
   static bool configured = false;
   if (!configured) {
@@ -366,7 +382,7 @@ int launch_tma_cfg(float* p, float* m, float* v, const uint16_t* g, uint16_t* w,
   }
   const int64_t cap = (int64_t)sm_count() * ctas_per_sm;
   const int64_t grid = ntiles < cap ? ntiles : cap;
-  k_adam_tma<GT, LT, NT, S><<<(unsigned)grid, NT, smem, st>>>(p, m, v, g, w, ntiles, s);
+  k_adam_tma<GT, LT, NT, S><<<(unsigned)grid, NT, smem, st>>>(p, m, v, g, w, ntiles, tail, s);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return DOS_OK;
 }
@@ -402,11 +418,11 @@ bool tma_enabled() {
 }
 
 template <int GT, int LT>
-int launch_adam_tma(float* p, float* m, float* v, const uint16_t* g, uint16_t* w, int64_t ntiles, const dos_kscal& s,
-                    cudaStream_t st) {
+int launch_adam_tma(float* p, float* m, float* v, const uint16_t* g, uint16_t* w, int64_t ntiles, int64_t tail,
+                    const dos_kscal& s, cudaStream_t st) {
   const TmaCfg& c = tma_cfg();
 #define DOS_CFG(NT_, S_) \
-  if (c.nt == NT_ && c.stages == S_) return launch_tma_cfg<GT, LT, NT_, S_>(p, m, v, g, w, ntiles, s, c.cpb, st);
+  if (c.nt == NT_ && c.stages == S_) return launch_tma_cfg<GT, LT, NT_, S_>(p, m, v, g, w, ntiles, tail, s, c.cpb, st);
   DOS_CFG(1024, 3)
   DOS_CFG(512, 6)
   DOS_CFG(256, 12)
@@ -450,7 +466,7 @@ int dos_adam_launch(float* p, float* m, float* v, const void* g, int gt, void* l
       (n - head) / (4 * tma_cfg().nt) >= 1) {
     const int64_t tile = 4 * tma_cfg().nt;
     const int64_t ntiles = (n - head) / tile;
-    const int64_t body_end = head + ntiles * tile;
+    const int64_t tail = n - head - ntiles * tile;  // < one tile; handled inside the same launch
     const char* gc = static_cast<const char*>(g);
     char* lc = static_cast<char*>(lp);
     int rc = DOS_OK;
@@ -459,16 +475,13 @@ int dos_adam_launch(float* p, float* m, float* v, const void* g, int gt, void* l
     const uint16_t* gb = reinterpret_cast<const uint16_t*>(gc + 2 * head);
     uint16_t* wb = lt == DOS_NONE ? nullptr : reinterpret_cast<uint16_t*>(lc + 2 * head);
 #define DOS_TMA(G, L) \
-  if (gt == G && lt == L) rc = launch_adam_tma<G, L>(p + head, m + head, v + head, gb, wb, ntiles, s, st);
+  if (gt == G && lt == L) rc = launch_adam_tma<G, L>(p + head, m + head, v + head, gb, wb, ntiles, tail, s, st);
     DOS_TMA(DOS_F16, DOS_NONE) else DOS_TMA(DOS_F16, DOS_F16) else DOS_TMA(DOS_F16, DOS_BF16)
     else DOS_TMA(DOS_BF16, DOS_NONE) else DOS_TMA(DOS_BF16, DOS_F16) else DOS_TMA(DOS_BF16, DOS_BF16)
 #undef DOS_TMA
     if (rc != DOS_OK) return rc;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return dos_set_error(DOS_ECUDA, "K1 (TMA) launch failed: %s", cudaGetErrorString(e));
-    if (body_end < n)
-      rc = dos_adam_launch(p + body_end, m + body_end, v + body_end, gc + 2 * body_end, gt,
-                           lt == DOS_NONE ? nullptr : static_cast<void*>(lc + 2 * body_end), lt, n - body_end, s, st);
     return rc;
   }
   int64_t nvec = 0;

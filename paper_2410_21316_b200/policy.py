@@ -19,7 +19,7 @@ import dataclasses
 from typing import Iterable, Sequence
 
 from .perfmodel import ALL_CPU
-from .plan import ActionKind, Device, Lane, UpdatePlan, build_plan
+from .plan import ActionKind, Device, Lane, ScheduledAction, UpdatePlan, build_plan
 from .state import SystemProfile
 from .timing import SimTarget, Timeline, build_timeline, normalize_sizes
 
@@ -80,25 +80,23 @@ def simulate_b200_phase(plan: UpdatePlan, profile: SystemProfile, subgroup_size:
     t = _B200Durations(profile, plan, sizes)
     lane_free = dict.fromkeys(Lane, 0)
     finish: list[int] = []
-    closes: list[int] = []  # window close times in opening order
+    closes: list[int] = []  # window close times, in opening order
+    window_of: dict[int, int] = {}  # subgroup -> index of its window in `closes`
     dyn = set(plan.dynamic_fast)
-    from .plan import ScheduledAction
-
     out = []
     for a in plan.actions:
         start = max([lane_free[a.lane], *(finish[d] for d in a.deps)])
         if a.kind is ActionKind.PREFETCH_M and a.subgroup in dyn:
             opened = len(closes)
-            if opened >= num_slots:
+            if opened >= num_slots:  # the slot frees when the window num_slots back closes
                 start = max(start, closes[opened - num_slots])
-            closes.append(-1)  # filled at FLUSH_OUT_P
-            t._win = getattr(t, "_win", {})
-            t._win[a.subgroup] = opened
+            closes.append(-1)  # filled at its FLUSH_OUT_P
+            window_of[a.subgroup] = opened
         end = start + t.duration_ns(a)
         finish.append(end)
         lane_free[a.lane] = end
         if a.kind is ActionKind.FLUSH_OUT_P and a.subgroup in dyn:
-            closes[t._win[a.subgroup]] = end
+            closes[window_of[a.subgroup]] = end
         out.append(ScheduledAction(action=a, start_ns=start, end_ns=end, bytes=t.bytes_of(a)))
     return build_timeline(plan, tuple(out), sizes)
 

@@ -30,6 +30,7 @@ from . import _native as N
 from .state import SystemProfile
 
 _OUT = Path(__file__).resolve().parent.parent / "profiles" / "b200_node_profile.json"
+LAST_RAW: dict = {}  # raw measurements behind the last measure_profile()
 
 
 def _torch():
@@ -126,12 +127,14 @@ def measure_h1(n: int = 100_000_000, with_dma: bool = False, reps: int = 3) -> d
     dma = None
     if with_dma:
         torch = _torch()
-        nb = 1 << 29
+        nb = 1 << 26  # 64 MB per direction per round: fine-grained byte accounting
         hx = torch.from_numpy(N.HostBuffer(nb).array(np.uint8, nb))
         hy = torch.from_numpy(N.HostBuffer(nb).array(np.uint8, nb))
         dx = torch.empty(nb, dtype=torch.uint8, device="cuda")
         dy = torch.empty(nb, dtype=torch.uint8, device="cuda")
         s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+        moved = [0]  # host bytes read + written by the copy engines
 
         def pump():
             while not stop.is_set():
@@ -141,6 +144,7 @@ def measure_h1(n: int = 100_000_000, with_dma: bool = False, reps: int = 3) -> d
                     hy.copy_(dy, non_blocking=True)
                 s1.synchronize()
                 s2.synchronize()
+                moved[0] += 2 * nb
 
         dma = threading.Thread(target=pump, daemon=True)
         dma.start()
@@ -149,14 +153,22 @@ def measure_h1(n: int = 100_000_000, with_dma: bool = False, reps: int = 3) -> d
                                                   N.DOS_BF16, w.ctypes.data, N.DOS_BF16, n, sc, 0))
     run()
     best = float("inf")
+    t_all0 = time.perf_counter()
+    moved0 = moved[0] if dma is not None else 0
     for _ in range(reps):
         t0 = time.perf_counter()
         run()
         best = min(best, time.perf_counter() - t0)
+    t_all = time.perf_counter() - t_all0
+    out = {"h1_params_per_s": n / best, "h1_GBs": 28 * n / best / 1e9, "threads": lib.dos_host_threads()}
     if dma is not None:
+        dma_bytes = moved[0] - moved0
         stop.set()
         dma.join()
-    return {"h1_params_per_s": n / best, "h1_GBs": 28 * n / best / 1e9, "threads": lib.dos_host_threads()}
+        # host DRAM bytes per second while H1 and duplex DMA share the memory
+        out["dma_GBs"] = dma_bytes / t_all / 1e9
+        out["host_dram_GBs_combined"] = (28 * n * reps + dma_bytes) / t_all / 1e9
+    return out
 
 
 def measure_profile(fast_capacity_bytes: int | None = None, save: bool = False, quick: bool = False) -> SystemProfile:
@@ -165,7 +177,7 @@ def measure_profile(fast_capacity_bytes: int | None = None, save: bool = False, 
     link = measure_link(1 << 28 if quick else 1 << 30)
     k1 = measure_k1(n)
     h1_alone = measure_h1(n)
-    h1_busy = measure_h1(n, with_dma=True)
+    h1_busy = measure_h1(100_000_000, with_dma=True)
     channel = min(link["duplex_GBs_per_dir"], link["h2d_GBs"], link["d2h_GBs"]) * 1e9 / 4.0
     contention = max(1.0, h1_alone["h1_params_per_s"] / h1_busy["h1_params_per_s"])
     prof = SystemProfile(
@@ -183,6 +195,8 @@ def measure_profile(fast_capacity_bytes: int | None = None, save: bool = False, 
         host_contention=contention,
         caveat="measured by profile_b200.measure_profile",
     )
+    LAST_RAW.clear()
+    LAST_RAW.update({"link": link, "k1": k1, "h1_alone": h1_alone, "h1_with_dma": h1_busy})
     if save:
         d = dataclasses.asdict(prof)
         d["raw"] = {"link": link, "k1": k1, "h1_alone": h1_alone, "h1_with_dma": h1_busy,
