@@ -30,7 +30,7 @@ from typing import Sequence
 import numpy as np
 
 from . import _native as N
-from .plan import KIND_CODE, LANE_CODE, ActionKind, ScheduledAction, UpdatePlan
+from .plan import KIND_CODE, LANE_CODE, ActionKind, Lane, ScheduledAction, UpdatePlan
 from .state import SUBGROUP_STATE_BYTES_PER_PARAM, ShardedOptimizer, SystemProfile, bias_corrections
 from .timing import SimTarget
 
@@ -233,9 +233,9 @@ class _PlanDescs:
         for a in plan.actions:
             d = self.descs[a.id]
             d.id = a.id
-            d.kind = KIND_CODE[a.kind]
+            d.kind = KIND_CODE[ActionKind(a.kind.value)]  # by value: reference plans work too
             d.subgroup = a.subgroup
-            d.lane = LANE_CODE[a.lane]
+            d.lane = LANE_CODE[Lane(a.lane.value)]
             d.is_static = 1 if (a.subgroup >= 0 and a.subgroup in plan.static_set) else 0
             deps = np.array(a.deps, dtype=np.int32)
             batch = np.array(a.batch, dtype=np.int32)

@@ -35,6 +35,13 @@ _STATE_MOVES = frozenset({
 })
 
 
+def kind_of(action) -> ActionKind:
+    """The action's kind as this package's enum — also for Action objects
+    built by the reference package (same string values, another enum class)."""
+    k = action.kind
+    return k if type(k) is ActionKind else ActionKind(k.value)
+
+
 def normalize_sizes(plan: UpdatePlan, subgroup_size: "int | Sequence[int]") -> tuple[int, ...]:
     if isinstance(subgroup_size, int):
         return (subgroup_size,) * plan.num_subgroups
@@ -60,12 +67,12 @@ class SimTarget:
         self._cpu_scale = 1.0 if plan.blocking else profile.host_contention
 
     def _params(self, a: Action) -> int:
-        if a.kind is ActionKind.CPU_DOWNSCALE:
+        if kind_of(a) is ActionKind.CPU_DOWNSCALE:
             return sum(self.sizes[j] for j in a.batch)
         return self.sizes[a.subgroup]
 
     def duration_ns(self, action: Action) -> int:
-        p, s, k = self.profile, self._params(action), action.kind
+        p, s, k = self.profile, self._params(action), kind_of(action)
         if k is ActionKind.CPU_UPDATE:
             return ceil_ns(s / p.cpu_update_params_per_s * self._cpu_scale)
         if k is ActionKind.GPU_UPDATE:
@@ -82,7 +89,7 @@ class SimTarget:
 
     def bytes_of(self, action: Action) -> int:
         """Algorithmic link bytes: 4 B/param per fp32 piece, 2 B for halves."""
-        k = action.kind
+        k = kind_of(action)
         if k in _STATE_MOVES:
             return 4 * self._params(action)
         if k in (ActionKind.H2D_PARAMS16, ActionKind.FLUSH_OUT_MODEL16):

@@ -171,3 +171,48 @@ def test_b200_policy_refit_and_choice(h100):
     assert prof.channel_params_per_s > 0 and prof.fast_update_params_per_s > 0
     k, spans = policy.choose_stride(prof, sizes)
     assert k in spans and spans[k] == min(spans.values())
+
+
+def _tampered(plan, actions):
+    import dataclasses as dc
+
+    return dc.replace(plan, actions=tuple(actions))
+
+
+def test_engine_rejects_structural_violations(h100):
+    """The native engine enforces EmulatedDevice's rules on real HBM slots
+    (executor.py:134-171): a fast update without its triplet, a flush of a
+    piece never staged and a double stage all raise, and the engine stays
+    usable afterwards."""
+    from paper_2410_21316_b200.plan import Action, ActionKind
+
+    opt = D.ShardedOptimizer.initialize(40_000, 10_000, seed=2, lowp="bf16")
+    plan = D.build_plan(4, 1)
+    acts = list(plan.actions)
+    # drop subgroup 0's PREFETCH_V: GPU_UPDATE 0 finds an incomplete window
+    bad = [a for a in acts if not (a.kind is ActionKind.PREFETCH_V and a.subgroup == 0)]
+    bad = [Action(i, a.kind, a.subgroup, a.lane, a.stream, a.batch,
+                  tuple(d if d < 1 else d - 1 for d in a.deps if d != 1)) for i, a in enumerate(bad)]
+    with pytest.raises(AssertionError):
+        D.execute_plan(opt, _tampered(plan, bad), h100, HYPER, validate_measured=False)
+    # double stage: PREFETCH_M of subgroup 0 twice
+    dup = acts[:1] + [Action(1, ActionKind.PREFETCH_M, 0, acts[0].lane, acts[0].stream)]
+    with pytest.raises(AssertionError):
+        D.execute_plan(opt, _tampered(plan, dup), h100, HYPER, validate_measured=False)
+    # the engine recovers: a valid phase on a fresh shard still matches the oracle
+    ok = D.ShardedOptimizer.initialize(40_000, 10_000, seed=2, lowp="bf16")
+    ok.residency = None
+    D.execute_plan(ok, plan, h100, HYPER)
+    assert digest(ok) == oracle_digest(40_000, 10_000, 2, "bf16")
+
+
+def test_throttled_mode_paces_but_matches(h100):
+    import time
+
+    opt = D.ShardedOptimizer.initialize(512, 256, seed=3)
+    t0 = time.perf_counter()
+    res = D.execute_plan(opt, D.build_plan(2, 2), h100, HYPER, mode=D.ExecMode.THROTTLED, throttle_scale=1e-7)
+    assert time.perf_counter() - t0 < 5.0 and res.mode is D.ExecMode.THROTTLED
+    assert digest(opt) == oracle_digest(512, 256, 3)
+    with pytest.raises(ValueError):
+        D.execute_plan(opt, D.build_plan(2, 2), h100, HYPER, mode=D.ExecMode.THROTTLED, throttle_scale=0.0)

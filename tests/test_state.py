@@ -152,3 +152,22 @@ def test_execute_plan_needs_a_gpu(h100):
         D.execute_plan(opt, D.build_plan(3, 2), h100, D.AdamHyper())
     with pytest.raises(RuntimeError, match="CUDA"):
         D.execute_plan(opt, D.build_plan(4, 2), h100, D.AdamHyper())
+
+
+def test_emulated_device_ledger():
+    dev = D.EmulatedDevice()
+    dev.stage(0, "m", np.zeros(4, np.float32))
+    with pytest.raises(AssertionError):
+        dev.stage(0, "m", np.zeros(4, np.float32))
+    dev.stage(0, "v", np.zeros(4, np.float32))
+    with pytest.raises(AssertionError):
+        dev.require_triplet(0)
+    dev.stage(0, "p", np.zeros(4, np.float32))
+    assert set(dev.require_triplet(0)) == {"m", "v", "p"}
+    with pytest.raises(AssertionError):
+        dev.unstage(3, "p")
+    with pytest.raises(AssertionError):
+        dev.assert_drained()
+    for piece in "mvp":
+        dev.unstage(0, piece)
+    dev.assert_drained()
