@@ -374,6 +374,23 @@ def main() -> None:
     phase_bound = max(bounds, key=bounds.get)
     phase_ideal = bounds[phase_bound]
 
+    # ---------------- iteration time = grad flush + update span (+ RS/AG at N>1):
+    # the host lane reads the bf16 grads of host-scheduled subgroups, so they
+    # are flushed D2H (pinned) before the phase (§8(f) row 1; in training this
+    # overlaps the backward pass — reported separately, not hidden)
+    cpu_sgs = [g for i, g in enumerate(opt.subgroups) if plan.devices[i] is D.Device.CPU]
+    dev_g16 = opt.residency.grads.view(torch.int16)
+    host_g16 = torch.from_numpy(opt._g.view(np.int16))
+    fl0, fl1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    fl0.record()
+    for g in cpu_sgs:
+        host_g16[g.start:g.stop].copy_(dev_g16[g.start:g.stop], non_blocking=True)
+    fl1.record()
+    torch.cuda.synchronize()
+    flush_ms = max_over_ranks(fl0.elapsed_time(fl1))
+    flush_bytes = 2 * sum(g.size for g in cpu_sgs)
+
     # ---------------- e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -520,6 +537,9 @@ def main() -> None:
                 "predicted_span_ms": results[0].timeline.span_ns / 1e6,
                 "lane_busy_ms_per_step": {k: v / 1e6 / len(results) for k, v in lane_busy.items()},
                 "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
+                "grad_flush_ms": flush_ms, "grad_flush_bytes": flush_bytes,
+                "iteration_update_ms": flush_ms + float(np.median(spans)) / 1e6
+                if collectives is None else collectives["iteration_update_ms"] + flush_ms,
             },
             "roofline": {"bound": "hbm", "achieved": k1_gbs, "peak": hbm_peak, "unit": "GB/s",
                          "frac": (k1_gbs / hbm_peak) if k1_gbs else None, "traffic": traffic,

@@ -216,3 +216,24 @@ def test_throttled_mode_paces_but_matches(h100):
     assert digest(opt) == oracle_digest(512, 256, 3)
     with pytest.raises(ValueError):
         D.execute_plan(opt, D.build_plan(2, 2), h100, HYPER, mode=D.ExecMode.THROTTLED, throttle_scale=0.0)
+
+
+@pytest.mark.parametrize("name,nsub,tail", [
+    ("7B/1", 70, 1.0), ("13B/1", 130, 1.0), ("13B/2", 65, 1.0), ("20B/4", 50, 1.0), ("20B/8", 25, 1.0),
+    ("70B/8", 88, 0.5),
+])
+def test_baseline_config_shapes(name, nsub, tail):
+    """Each BASELINE config's per-rank shard shape (subgroup count, ragged
+    last subgroup) at a scaled-down subgroup size, with the planner's measured
+    B200 profile and the policy's stride, bit-exact against the oracle."""
+    from paper_2410_21316_b200 import policy
+
+    sg = 20_000
+    total = (nsub - 1) * sg + int(tail * sg)
+    prof = D.get_profile("b200-node")
+    sizes = [sg] * (nsub - 1) + [int(tail * sg)]
+    stride, _ = policy.choose_stride(prof, sizes, range(1, 7), 0.2)
+    for ratio, k in ((0.0, stride), (0.2, stride), (0.0, D.optimal_stride(prof, nsub, sg).k)):
+        opt = D.ShardedOptimizer.initialize(total, sg, seed=nsub, lowp="bf16")
+        D.execute_plan(opt, D.build_plan(nsub, k, static_ratio=ratio), prof, HYPER)
+        assert digest(opt) == oracle_digest(total, sg, nsub, "bf16"), (name, ratio, k)
