@@ -44,7 +44,11 @@ def _torch():
 class DeviceResidency:
     """What of one ShardedOptimizer lives in HBM, and host/device coherence."""
 
-    def __init__(self, opt: ShardedOptimizer, device=None) -> None:
+    def __init__(self, opt: ShardedOptimizer, device=None, grads=None, model16=None) -> None:
+        """``grads``/``model16`` may be caller-owned CUDA views (e.g. this
+        rank's chunk of a full-model buffer, so the phase writes the model's
+        parameters in place); otherwise they are allocated here.  Their
+        current contents are replaced by the host images."""
         torch = _torch()
         if not torch.cuda.is_available():
             raise RuntimeError("no CUDA device visible: the B200 update phase needs a GPU (no CPU fallback)")
@@ -56,9 +60,13 @@ class DeviceResidency:
         self.tdtype = torch.float16 if opt.lowp == "fp16" else torch.bfloat16
         P = opt.total_params
         nsg = len(opt.subgroups)
+        for name, t in (("grads", grads), ("model16", model16)):
+            if t is not None and (t.dtype != self.tdtype or t.numel() != P or not t.is_contiguous()
+                                  or t.device != self.device):
+                raise ValueError(f"{name} must be a contiguous {self.tdtype} tensor of {P} elements on {self.device}")
         with torch.cuda.device(self.device):
-            self.grads = torch.empty(P, dtype=self.tdtype, device=self.device)
-            self.model16 = torch.empty(P, dtype=self.tdtype, device=self.device)
+            self.grads = grads if grads is not None else torch.empty(P, dtype=self.tdtype, device=self.device)
+            self.model16 = model16 if model16 is not None else torch.empty(P, dtype=self.tdtype, device=self.device)
         self.sg_start = np.array([g.start for g in opt.subgroups], dtype=np.int64)
         self.sg_size = np.array([g.size for g in opt.subgroups], dtype=np.int64)
         self.static_set: frozenset[int] = frozenset()

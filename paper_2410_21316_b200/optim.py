@@ -1,20 +1,26 @@
 """A torch-optimizer-style ``step()`` over the B200 update phase.
 
 ``DeepOptimizerStates(params, ...)`` flattens a model's half-precision CUDA
-parameters into one shard and re-points every parameter (``.data``) and its
-``.grad`` at views of the residency's flat HBM buffers, so
+parameters into one padded full-model buffer and re-points every parameter
+(``.data``) and its ``.grad`` at views of it, so
 
 * backward accumulates straight into the flat grad buffer (no copy);
-* the update phase's working-copy stores (K1 for fast subgroups,
-  H2D_PARAMS16 for host subgroups) *are* the model's parameters: no
-  all-params copy after the step.
+* this rank's chunk of the flat param buffer *is* the residency's working
+  copy: the phase's K1 / H2D_PARAMS16 stores update the model in place.
 
-fp32 master params (exact widening of the initial half-precision params,
-or caller-provided), Adam m and v live in the pinned host pool.  Each
-``step()``: flush the grads of host-scheduled subgroups D2H (the §8(f) row-1
-gradient path), run ``execute_plan`` on the current plan, then re-fit the
-machine profile from the measured timeline and re-choose the stride
-(the per-iteration split of the north star).
+One process per GPU.  With ``process_group`` of N ranks the state is
+ZeRO-3 sharded (``shard(P, N, SG)``, core.py:139-170): each rank keeps the
+fp32 master params, Adam m and v of its own chunk in its pinned host pool,
+and ``step()`` runs
+
+1. a bucketed reduce-scatter of the bf16 grads into this rank's chunk
+   (summed; ``average_grads`` divides by N),
+2. the D2H flush of the grads the host lane will read (§8(f) row 1),
+3. the update phase (``execute_plan``), with every bucket's all-gather of
+   the working copy chained onto the engine event that finalises its
+   subgroup (``distributed.gather_params_overlapped``),
+4. a per-iteration re-fit: explore-then-exploit over strides by measured
+   span (``policy.StrideTuner``), identical on every rank.
 """
 
 from __future__ import annotations
@@ -22,16 +28,18 @@ from __future__ import annotations
 import numpy as np
 
 from . import policy
+from .distributed import BucketedCollectives, ShardLayout, gather_params_overlapped
 from .executor import AdamHyper, execute_plan
 from .plan import Device, build_plan
-from .state import ShardedOptimizer
+from .state import ShardedOptimizer, lowp_downscale
 
 
 class DeepOptimizerStates:
     def __init__(self, params, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 0.0,
                  *, subgroup_size: int = 100_000_000, profile=None, stride="auto", static_ratio: float = 0.0,
-                 master_params=None, replan: bool = True) -> None:
+                 master_params=None, process_group=None, average_grads: bool = False, explore: int = 3) -> None:
         import torch
+        import torch.distributed as dist
 
         self.params = [p for p in params if p.requires_grad]
         if not self.params:
@@ -41,47 +49,64 @@ class DeepOptimizerStates:
             raise TypeError("parameters must all be CUDA bfloat16 or all CUDA float16")
         self.lowp = "bf16" if dt == torch.bfloat16 else "fp16"
         self.hyper = AdamHyper(lr=lr, beta1=betas[0], beta2=betas[1], eps=eps, weight_decay=weight_decay)
-        total = sum(p.numel() for p in self.params)
-        sg = min(int(subgroup_size), total)
-        opt = ShardedOptimizer.allocate(total, sg, lowp=self.lowp)
+        self.group = process_group
+        self.world = dist.get_world_size(process_group) if process_group is not None else 1
+        self.rank = dist.get_rank(process_group) if process_group is not None else 0
+        self.average_grads = average_grads
         dev = self.params[0].device
+        total = sum(p.numel() for p in self.params)
+        sg = min(int(subgroup_size), -(-total // self.world))
+        self.layout = lay = ShardLayout.build(total, self.world, sg)
+        self.offset = self.rank * lay.per_rank
+        mine = sum(g.size for g in lay.ranks[self.rank])
+
+        # full-model flat buffers (padded), params and grads re-pointed into them
+        self.flat = torch.zeros(lay.padded_total, dtype=dt, device=dev)
+        self.flat_grad = torch.zeros(lay.padded_total, dtype=dt, device=dev)
         off = 0
         with torch.no_grad():
             for p in self.params:
                 n = p.numel()
-                src = p.detach().reshape(-1)
-                if master_params is None:
-                    torch.from_numpy(opt._p[off:off + n]).copy_(src.float())  # exact widening
-                opt._w[off:off + n] = src.view(torch.int16).cpu().numpy().view(opt._w.dtype)
+                self.flat[off:off + n].copy_(p.detach().reshape(-1))
+                p.data = self.flat[off:off + n].view(p.shape)
+                p.grad = self.flat_grad[off:off + n].view(p.shape)
                 off += n
-            if master_params is not None:
-                flat = torch.cat([m.detach().reshape(-1).float().cpu() for m in master_params])
-                if flat.numel() != total:
-                    raise ValueError("master_params must match params element for element")
-                opt._p[:] = flat.numpy()
+
+        opt = ShardedOptimizer.allocate(mine, sg, lowp=self.lowp)
+        chunk = self.flat[self.offset:self.offset + mine]
+        if master_params is None:
+            torch.from_numpy(opt._p).copy_(chunk.float())  # exact widening
+        else:
+            flat_m = torch.cat([m.detach().reshape(-1).float().cpu() for m in master_params])
+            if flat_m.numel() != total:
+                raise ValueError("master_params must match params element for element")
+            opt._p[:] = flat_m[self.offset:self.offset + mine].numpy()
+            with torch.no_grad():  # working copy = RNE of the masters
+                chunk.copy_(torch.from_numpy(lowp_downscale(opt._p, self.lowp).view(np.int16)).view(dt))
+        opt._w[:] = chunk.view(torch.int16).cpu().numpy().view(opt._w.dtype)
         opt._m[:] = 0
         opt._v[:] = 0
         opt._g[:] = 0
         self.opt = opt
-        self.res = opt.to_device(dev)
-        # re-point params and grads at the flat HBM buffers
-        off = 0
-        for p in self.params:
-            n = p.numel()
-            p.data = self.res.model16[off:off + n].view(p.shape)
-            p.grad = self.res.grads[off:off + n].view(p.shape)
-            off += n
+        self.res = opt.to_device(dev, grads=self.flat_grad[self.offset:self.offset + mine], model16=chunk)
+        self.coll = BucketedCollectives(lay, process_group) if self.world > 1 else None
+
         if profile is None:
             from .catalog import get_profile
 
             profile = get_profile("b200-node")
         self.profile = profile
         self.static_ratio = static_ratio
-        self.replan = replan and stride == "auto"
-        sizes = [g.size for g in opt.subgroups]
+        self.sizes = [g.size for g in opt.subgroups]
+        self.tuner = None
         if stride == "auto":
-            stride, _ = policy.choose_stride(profile, sizes, range(1, 7), static_ratio)
-        self.plan = build_plan(len(sizes), stride, static_ratio=static_ratio)
+            self.tuner = policy.StrideTuner(profile, self.sizes, range(1, 7), static_ratio, explore=explore)
+            if self.world > 1:  # the same exploration order on every rank
+                box = [self.tuner.queue]
+                dist.broadcast_object_list(box, src=0, group=process_group)
+                self.tuner.queue = list(box[0])
+            stride = self.tuner.next_stride()
+        self.plan = build_plan(len(self.sizes), stride, static_ratio=static_ratio)
         self.last = None
 
     @property
@@ -91,7 +116,12 @@ class DeepOptimizerStates:
     def zero_grad(self, set_to_none: bool = False) -> None:
         if set_to_none:
             raise ValueError("grads are views of the flat HBM buffer; use zero_grad(set_to_none=False)")
-        self.res.grads.zero_()
+        self.flat_grad.zero_()
+
+    def _reduce_grads(self) -> None:
+        lay = self.layout
+        own = self.flat_grad[self.offset:self.offset + lay.per_rank]
+        self.coll.reduce_scatter_all(self.flat_grad, own, scale=1.0 / self.world if self.average_grads else None)
 
     def _flush_host_grads(self) -> None:
         """D2H of the grads the host lane will read (CPU subgroups only)."""
@@ -104,35 +134,57 @@ class DeepOptimizerStates:
                 host[sg.start:sg.stop].copy_(g[sg.start:sg.stop], non_blocking=True)
         torch.cuda.current_stream(self.res.device).synchronize()
 
+    def _max_over_ranks(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        import torch
+        import torch.distributed as dist
+
+        t = torch.tensor([x], dtype=torch.float64)
+        if dist.get_backend(self.group) == "nccl":
+            t = t.to(self.res.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
     def step(self):
         import torch
 
         torch.cuda.current_stream(self.res.device).synchronize()  # backward done
+        if self.coll is not None:
+            self._reduce_grads()
+            torch.cuda.current_stream(self.res.device).synchronize()
         self._flush_host_grads()
-        self.last = execute_plan(self.opt, self.plan, self.profile, self.hyper)
-        if self.replan and self.last.measured is not None:
-            sizes = [g.size for g in self.opt.subgroups]
-            self.profile = policy.refit_profile(self.profile, self.last.measured, sizes)
-            stride, _ = policy.choose_stride(self.profile, sizes, range(1, 7), self.static_ratio)
-            if stride != self.plan.stride:
-                self.plan = build_plan(len(sizes), stride, static_ratio=self.static_ratio)
+        hook = gather_params_overlapped(self.coll, self.plan, self.res.model16, self.flat) \
+            if self.coll is not None else None
+        self.last = execute_plan(self.opt, self.plan, self.profile, self.hyper, on_submitted=hook)
+        if hook is not None:
+            for w in hook.works:
+                if w is not None:
+                    w.wait()
+            torch.cuda.current_stream(self.res.device).wait_stream(hook.stream)
+        if self.tuner is not None and self.last.measured is not None:
+            self.tuner.record(self.plan.stride, int(self._max_over_ranks(self.last.measured.span_ns)))
+            nxt = self.tuner.next_stride()
+            if nxt != self.plan.stride:
+                self.plan = build_plan(len(self.sizes), nxt, static_ratio=self.static_ratio)
         return self.last
 
     def master_params(self) -> np.ndarray:
-        """fp32 master params (host image, synchronised)."""
+        """This rank's fp32 master params (host image, synchronised)."""
         return self.opt.params32
 
     def state_dict(self) -> dict:
-        return {"step": self.opt.step, "params32": self.opt.params32.copy(), "momentum32": self.opt.momentum32.copy(),
-                "variance32": self.opt.variance32.copy(), "hyper": self.hyper, "stride": self.plan.stride}
+        return {"step": self.opt.step, "rank": self.rank, "world": self.world, "offset": self.offset,
+                "params32": self.opt.params32.copy(), "momentum32": self.opt.momentum32.copy(),
+                "variance32": self.opt.variance32.copy(), "hyper": self.hyper}
 
     def load_state_dict(self, sd: dict) -> None:
+        if (sd.get("rank", 0), sd.get("world", 1)) != (self.rank, self.world):
+            raise ValueError("state dict belongs to another rank / world size")
         self.res.sync_all_host()
         self.opt._p[:] = sd["params32"]
         self.opt._m[:] = sd["momentum32"]
         self.opt._v[:] = sd["variance32"]
         self.opt.step = int(sd["step"])
-        from .state import lowp_downscale
-
         self.opt._w[:] = lowp_downscale(self.opt._p, self.lowp)
         self.res.push_host()

@@ -395,12 +395,13 @@ class ShardedOptimizer:
         return all(a.view(np.uint8).tobytes() == b.view(np.uint8).tobytes() for a, b in pairs)
 
     # -- device attachment
-    def to_device(self, device=None) -> "DeviceResidency":
-        """Attach (or return) the B200 residency: grads + working copy in HBM."""
+    def to_device(self, device=None, grads=None, model16=None) -> "DeviceResidency":
+        """Attach (or return) the B200 residency: grads + working copy in HBM
+        (optionally in caller-owned CUDA views, see DeviceResidency)."""
         from .device import DeviceResidency
 
         if self.residency is None:
-            self.residency = DeviceResidency(self, device)
+            self.residency = DeviceResidency(self, device, grads=grads, model16=model16)
         return self.residency
 
     def load_grads(self, grads) -> None:

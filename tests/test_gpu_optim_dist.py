@@ -1,0 +1,84 @@
+"""ZeRO-3 DeepOptimizerStates with two ranks sharing the box's one B200
+(gloo process group, CUDA tensors): reduce-scatter -> sharded update phase
+-> overlapped all-gather.  Every rank's shard must equal the oracle's Adam on
+(its master chunk, its reduced grads), and all ranks must end with identical
+full-model params."""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def _port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, stride, q):
+    try:
+        import torch.distributed as dist
+
+        from oracle import optistate_oracle as O
+        from paper_2410_21316_b200 import get_profile
+        from paper_2410_21316_b200.optim import DeepOptimizerStates
+
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.manual_seed(0)  # identical initial model on every rank
+        model = torch.nn.Sequential(torch.nn.Linear(128, 300), torch.nn.GELU(), torch.nn.Linear(300, 50)).cuda().to(
+            torch.bfloat16)
+        init = torch.cat([p.detach().reshape(-1) for p in model.parameters()]).float().cpu().numpy().copy()
+        opt = DeepOptimizerStates(model.parameters(), lr=1e-3, subgroup_size=9_000, profile=get_profile("h100-node"),
+                                  stride=stride, static_ratio=0.2, process_group=dist.group.WORLD)
+        lay, off = opt.layout, opt.offset
+        mine = opt.opt.total_params
+        st = {"p": init[off:off + mine].copy(), "m": np.zeros(mine, np.float32), "v": np.zeros(mine, np.float32),
+              "w": None, "g": None, "subgroups": O.shard_subgroups(mine, lay.subgroup_size), "step": 0, "lowp": "bf16"}
+        st["w"] = O.bf16_from_f32(st["p"])
+        torch.manual_seed(100 + rank)  # different data per rank
+        ok = True
+        for _ in range(3):
+            opt.zero_grad()
+            x = torch.randn(16, 128, device="cuda", dtype=torch.bfloat16)
+            model(x).float().pow(2).mean().backward()
+            opt.step()
+            st["g"] = opt.res.grads.view(torch.int16).cpu().numpy().view(np.uint16).copy()  # post reduce-scatter
+            O.sequential_oracle(st)
+            ok &= opt.master_params().tobytes() == st["p"].tobytes()
+            ok &= opt.res.model16.view(torch.int16).cpu().numpy().view(np.uint16).tobytes() == st["w"].tobytes()
+            full = opt.flat.view(torch.int16).cpu()
+            gathered = [torch.zeros_like(full) for _ in range(world)]
+            dist.all_gather(gathered, full)
+            ok &= all(torch.equal(gathered[0], g) for g in gathered[1:])
+        q.put((rank, bool(ok), opt.plan.stride))
+        dist.destroy_process_group()
+    except Exception as e:  # report instead of hanging the parent
+        import traceback
+
+        q.put((rank, False, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("stride", [2, "auto"])
+def test_two_rank_zero3_step_matches_oracle(stride):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, stride, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok, _ in res), res
