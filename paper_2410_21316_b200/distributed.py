@@ -100,21 +100,32 @@ class BucketedCollectives:
         views = self._views(full_grads, j)
         if self.backend == "nccl":
             return dist.reduce_scatter(out, views, op=op, group=self.group, async_op=True)
-        # gloo: no reduce-scatter; all-reduce the bucket and keep our piece
+        # gloo: no reduce-scatter and no 16-bit float support; all-reduce the
+        # bucket in fp32 (exact widening, one rounding back) and keep our piece
         buf = torch.cat(views)
-        dist.all_reduce(buf, op=op, group=self.group)
+        wide = buf.float() if buf.element_size() == 2 else buf
+        dist.all_reduce(wide, op=op, group=self.group)
         size = views[0].numel()
-        out.copy_(buf[self.rank * size:(self.rank + 1) * size])
+        out.copy_(wide[self.rank * size:(self.rank + 1) * size].to(out.dtype))
         return None
 
     def all_gather_bucket(self, full_params, mine, j: int):
         """Every rank's piece of bucket j into the full-model buffer."""
+        import torch
         import torch.distributed as dist
 
         views = self._views(full_params, j)
         if self.backend == "nccl":
             return dist.all_gather(views, mine, group=self.group, async_op=True)
-        dist.all_gather(views, mine.contiguous(), group=self.group)
+        # gloo: gather exactly-widened fp32 copies (16-bit floats unsupported)
+        src = mine.contiguous()
+        if src.element_size() == 2 and src.is_floating_point():
+            wide = [torch.empty(v.numel(), dtype=torch.float32, device=v.device) for v in views]
+            dist.all_gather(wide, src.float(), group=self.group)
+            for v, w in zip(views, wide):
+                v.copy_(w.to(v.dtype))
+        else:
+            dist.all_gather(views, src, group=self.group)
         return None
 
     def reduce_scatter_all(self, full_grads, shard_grads, scale: float | None = None):

@@ -56,7 +56,7 @@ def _worker(rank, world, port, stride, q):
             O.sequential_oracle(st)
             ok &= opt.master_params().tobytes() == st["p"].tobytes()
             ok &= opt.res.model16.view(torch.int16).cpu().numpy().view(np.uint16).tobytes() == st["w"].tobytes()
-            full = opt.flat.view(torch.int16).cpu()
+            full = opt.flat.view(torch.int16).cpu().to(torch.int32)
             gathered = [torch.zeros_like(full) for _ in range(world)]
             dist.all_gather(gathered, full)
             ok &= all(torch.equal(gathered[0], g) for g in gathered[1:])
