@@ -72,6 +72,23 @@ int dos_adam_step_cuda(float* p, float* m, float* v, const void* g, int g_dtype,
                        void* p_lowp, int lowp_dtype, int64_t n,
                        const dos_adam_scalars* s, void* stream);
 
+/* K1 with the all-gather fused into its epilogue: as dos_adam_step_cuda,
+ * and every updated half-precision element is also stored to peer_lowp[r]
+ * (r < npeers <= DOS_MAX_PEERS), e.g. NVLink-mapped peer buffers.
+ * Replaces executor.py:219-227 FLUSH_OUT_MODEL16 + the ZeRO-3 param
+ * all-gather; requires lowp_dtype != DOS_NONE. */
+int dos_adam_step_cuda_bcast(float* p, float* m, float* v, const void* g, int g_dtype,
+                             void* p_lowp, int lowp_dtype, void* const* peer_lowp, int npeers,
+                             int64_t n, const dos_adam_scalars* s, void* stream);
+
+/* ---- CUDA IPC for symmetric full-model buffers (one process per GPU).
+ * export: the handle of the allocation containing dev_ptr and dev_ptr's
+ * byte offset in it; import: map a peer's allocation (cached) and return
+ * base + offset; close: unmap everything this process imported. */
+int dos_ipc_export(const void* dev_ptr, unsigned char handle[64], uint64_t* offset);
+int dos_ipc_import(const unsigned char handle[64], uint64_t offset, void** dev_ptr);
+int dos_ipc_close_all(void);
+
 /* ---- H1: the same update on host cores (bit-identical results).  Blocks
  * the calling thread only; nthreads <= 0 uses the library's host team. */
 int dos_adam_step_host(float* p, float* m, float* v, const void* g, int g_dtype,
@@ -138,7 +155,17 @@ typedef struct dos_state_desc {
    * and their working copy D2H inside FLUSH_OUT_P (static: inside
    * FLUSH_OUT_MODEL16), so the extra 2+2 B/param ride the same lanes. */
   int32_t host_io;
+  /* Fused all-gather of the working copy (ZeRO-3, one node).  peer_lowp[r]
+   * is where THIS rank's shard starts inside peer r's full-model buffer
+   * (an IPC-mapped NVLink address, see dos_ipc_*).  K1 stores each updated
+   * half-precision element to the local working copy and to every peer in
+   * the same pass; a host subgroup's working copy is forwarded peer-to-peer
+   * by the copy engine right after its H2D_PARAMS16.  npeers <= DOS_MAX_PEERS. */
+  int32_t npeers;
+  void* const* peer_lowp;
 } dos_state_desc;
+
+#define DOS_MAX_PEERS 7
 
 typedef struct dos_exec_config {
   int32_t device;

@@ -74,7 +74,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         o = BUILD / "dos_cuda.o"
         _run([NVCC, *NVCCFLAGS, "-c", str(CSRC / "dos_cuda.cu"), "-o", str(o)], log)
         objs.append(o)
-        for name in ("dos_host", "dos_exec"):
+        for name in ("dos_host", "dos_exec", "dos_ipc"):
             o = BUILD / f"{name}.o"
             _run(["g++", *CXXFLAGS, "-c", str(CSRC / f"{name}.cpp"), "-o", str(o)], log)
             objs.append(o)

@@ -55,7 +55,12 @@ class dos_state_desc(C.Structure):
         ("dev_g", C.c_void_p), ("dev_lowp", C.c_void_p),
         ("dev_static_p", C.c_void_p), ("dev_static_m", C.c_void_p), ("dev_static_v", C.c_void_p),
         ("host_io", C.c_int32),
+        ("npeers", C.c_int32),
+        ("peer_lowp", C.POINTER(C.c_void_p)),
     ]
+
+
+DOS_MAX_PEERS = 7
 
 
 class dos_exec_config(C.Structure):
@@ -81,6 +86,11 @@ SIGNATURES: dict[str, tuple] = {
     "dos_launch_count": (_I64, []),
     "dos_adam_step_cuda": (_I, [_VP, _VP, _VP, _VP, _I, _VP, _I, _I64, C.POINTER(dos_adam_scalars), _VP]),
     "dos_adam_step_host": (_I, [_VP, _VP, _VP, _VP, _I, _VP, _I, _I64, C.POINTER(dos_adam_scalars), _I]),
+    "dos_adam_step_cuda_bcast": (_I, [_VP, _VP, _VP, _VP, _I, _VP, _I, C.POINTER(_VP), _I, _I64,
+                                      C.POINTER(dos_adam_scalars), _VP]),
+    "dos_ipc_export": (_I, [_VP, C.c_char_p, C.POINTER(C.c_uint64)]),
+    "dos_ipc_import": (_I, [C.c_char_p, C.c_uint64, C.POINTER(_VP)]),
+    "dos_ipc_close_all": (_I, []),
     "dos_downscale_host": (_I, [_VP, _VP, _I, _I64, _I]),
     "dos_upscale_host": (_I, [_VP, _I, _VP, _I64, _I]),
     "dos_downscale_cuda": (_I, [_VP, _VP, _I, _I64, _VP]),

@@ -71,7 +71,7 @@ template <int GT, int LT>
 __global__ void __launch_bounds__(kThreads)
     k_adam(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
            const void* __restrict__ g, void* __restrict__ lp, int64_t head, int64_t nvec,
-           int64_t n, dos_kscal s) {
+           int64_t n, dos_kscal s, dos_peers pr) {
   const int64_t tid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   const int64_t nthr = (int64_t)gridDim.x * kThreads;
 
@@ -106,7 +106,9 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
       for (int k = 0; k < 4; ++k)
         w[k] = (uint32_t)to_lowp(pe[2 * k], LT) | ((uint32_t)to_lowp(pe[2 * k + 1], LT) << 16);
-      __stcs(reinterpret_cast<uint4*>(lv) + i, make_uint4(w[0], w[1], w[2], w[3]));
+      const uint4 wv = make_uint4(w[0], w[1], w[2], w[3]);
+      __stcs(reinterpret_cast<uint4*>(lv) + i, wv);
+      for (int r = 0; r < pr.n; ++r) reinterpret_cast<uint4*>(pr.p[r] + head)[i] = wv;  // fused all-gather
     }
   }
 
@@ -120,7 +122,11 @@ __global__ void __launch_bounds__(kThreads)
     p[e] = pe;
     m[e] = me;
     v[e] = ve;
-    if (LT != DOS_NONE) reinterpret_cast<uint16_t*>(lp)[e] = to_lowp(pe, LT);
+    if (LT != DOS_NONE) {
+      const uint16_t wb = to_lowp(pe, LT);
+      reinterpret_cast<uint16_t*>(lp)[e] = wb;
+      for (int r = 0; r < pr.n; ++r) pr.p[r][e] = wb;
+    }
   }
 }
 
@@ -210,7 +216,7 @@ unsigned grid_for(int64_t work) {
 
 template <int GT, int LT>
 void launch_adam(float* p, float* m, float* v, const void* g, void* lp, int64_t head, int64_t nvec,
-                 int64_t n, const dos_kscal& s, cudaStream_t st) {
+                 int64_t n, const dos_kscal& s, cudaStream_t st, const dos_peers& pr) {
   const int64_t work = nvec > 0 ? nvec : n;
   static int cap_blocks = 0;  // resident CTAs per SM for this instantiation
   if (!cap_blocks) {
@@ -221,7 +227,7 @@ void launch_adam(float* p, float* m, float* v, const void* g, void* lp, int64_t 
   const int64_t cap = (int64_t)sm_count() * cap_blocks;
   int64_t want = (work + kThreads - 1) / kThreads;
   want = want < 1 ? 1 : (want < cap ? want : cap);
-  k_adam<GT, LT><<<(unsigned)want, kThreads, 0, st>>>(p, m, v, g, lp, head, nvec, n, s);
+  k_adam<GT, LT><<<(unsigned)want, kThreads, 0, st>>>(p, m, v, g, lp, head, nvec, n, s, pr);
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
@@ -284,7 +290,7 @@ template <int GT, int LT, int NT, int S>
 __global__ void __launch_bounds__(NT, 1)
     k_adam_tma(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
                const uint16_t* __restrict__ g, uint16_t* __restrict__ w, int64_t ntiles, int64_t tail,
-               dos_kscal s) {
+               dos_kscal s, dos_peers pr) {
   constexpr int TE = 4 * NT;  // 4 elements per thread per tile
   constexpr uint32_t F32B = TE * 4, H16B = TE * 2, STAGE = 3 * F32B + H16B;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -333,9 +339,15 @@ __global__ void __launch_bounds__(NT, 1)
     *P = make_float4(pe[0], pe[1], pe[2], pe[3]);
     *M = make_float4(me[0], me[1], me[2], me[3]);
     *V = make_float4(ve[0], ve[1], ve[2], ve[3]);
-    if (LT != DOS_NONE)
-      *G = make_uint2((uint32_t)to_lowp(pe[0], LT) | ((uint32_t)to_lowp(pe[1], LT) << 16),
-                      (uint32_t)to_lowp(pe[2], LT) | ((uint32_t)to_lowp(pe[3], LT) << 16));
+    if (LT != DOS_NONE) {
+      const uint2 wv = make_uint2((uint32_t)to_lowp(pe[0], LT) | ((uint32_t)to_lowp(pe[1], LT) << 16),
+                                  (uint32_t)to_lowp(pe[2], LT) | ((uint32_t)to_lowp(pe[3], LT) << 16));
+      *G = wv;
+      // fused all-gather: the same 8 bytes straight into every peer's copy
+      // (NVLink stores through IPC-mapped addresses), coalesced per warp
+      const int64_t e0 = (first + k * step) * TE;
+      for (int r = 0; r < pr.n; ++r) reinterpret_cast<uint2*>(pr.p[r] + e0)[tid] = wv;
+    }
     fence_async_smem();  // generic-proxy smem writes -> visible to the bulk-copy (async) proxy
     __syncthreads();
     if (tid == 0) {
@@ -363,7 +375,11 @@ __global__ void __launch_bounds__(NT, 1)
       p[e] = pe;
       m[e] = me;
       v[e] = ve;
-      if (LT != DOS_NONE) w[e] = to_lowp(pe, LT);
+      if (LT != DOS_NONE) {
+        const uint16_t wb = to_lowp(pe, LT);
+        w[e] = wb;
+        for (int r = 0; r < pr.n; ++r) pr.p[r][e] = wb;
+      }
     }
   }
   if (tid == 0) bulk_wait_all();
@@ -371,7 +387,7 @@ __global__ void __launch_bounds__(NT, 1)
 
 template <int GT, int LT, int NT, int S>
 int launch_tma_cfg(float* p, float* m, float* v, const uint16_t* g, uint16_t* w, int64_t ntiles, int64_t tail,
-                   const dos_kscal& s, int ctas_per_sm, cudaStream_t st) {
+                   const dos_kscal& s, int ctas_per_sm, cudaStream_t st, const dos_peers& pr) {
   constexpr int smem = S * 4 * NT * 14;
   static bool configured = false;
   if (!configured) {
@@ -382,7 +398,7 @@ int launch_tma_cfg(float* p, float* m, float* v, const uint16_t* g, uint16_t* w,
   }
   const int64_t cap = (int64_t)sm_count() * ctas_per_sm;
   const int64_t grid = ntiles < cap ? ntiles : cap;
-  k_adam_tma<GT, LT, NT, S><<<(unsigned)grid, NT, smem, st>>>(p, m, v, g, w, ntiles, tail, s);
+  k_adam_tma<GT, LT, NT, S><<<(unsigned)grid, NT, smem, st>>>(p, m, v, g, w, ntiles, tail, s, pr);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return DOS_OK;
 }
@@ -419,10 +435,11 @@ bool tma_enabled() {
 
 template <int GT, int LT>
 int launch_adam_tma(float* p, float* m, float* v, const uint16_t* g, uint16_t* w, int64_t ntiles, int64_t tail,
-                    const dos_kscal& s, cudaStream_t st) {
+                    const dos_kscal& s, cudaStream_t st, const dos_peers& pr) {
   const TmaCfg& c = tma_cfg();
 #define DOS_CFG(NT_, S_) \
-  if (c.nt == NT_ && c.stages == S_) return launch_tma_cfg<GT, LT, NT_, S_>(p, m, v, g, w, ntiles, tail, s, c.cpb, st);
+  if (c.nt == NT_ && c.stages == S_)  \
+    return launch_tma_cfg<GT, LT, NT_, S_>(p, m, v, g, w, ntiles, tail, s, c.cpb, st, pr);
   DOS_CFG(1024, 3)
   DOS_CFG(512, 6)
   DOS_CFG(256, 12)
@@ -455,12 +472,23 @@ dos_kscal dos_make_kscal(const dos_adam_scalars* s) {
   return k;
 }
 
+dos_peers dos_peers_offset(const dos_peers& pr, int64_t elems) {
+  dos_peers o = pr;
+  for (int r = 0; r < pr.n; ++r) o.p[r] = pr.p[r] + elems;
+  return o;
+}
+
 int dos_adam_launch(float* p, float* m, float* v, const void* g, int gt, void* lp, int lt, int64_t n,
-                    const dos_kscal& s, cudaStream_t st) {
+                    const dos_kscal& s, cudaStream_t st, const dos_peers& pr) {
   if (n == 0) return DOS_OK;
-  const void* ptrs[5] = {p, m, v, g, lp};
-  const int eb[5] = {4, 4, 4, gt == DOS_F32 ? 4 : 2, 2};
-  int64_t head = common_head(ptrs, eb, lt == DOS_NONE ? 4 : 5, n);
+  if (pr.n > 0 && lt == DOS_NONE) return dos_set_error(DOS_EINVAL, "peer broadcast needs a working-copy dtype");
+  const void* ptrs[5 + DOS_MAX_PEERS] = {p, m, v, g, lp};
+  int eb[5 + DOS_MAX_PEERS] = {4, 4, 4, gt == DOS_F32 ? 4 : 2, 2};
+  for (int r = 0; r < pr.n; ++r) {  // peers share the 16-byte phase of the local stores
+    ptrs[5 + r] = pr.p[r];
+    eb[5 + r] = 2;
+  }
+  int64_t head = common_head(ptrs, eb, lt == DOS_NONE ? 4 : 5 + pr.n, n);
   // TMA path: 16-bit grads, a 16-byte-alignable range of at least one tile.
   if (gt != DOS_F32 && (lt == DOS_NONE || lt == DOS_F16 || lt == DOS_BF16) && head >= 0 && tma_enabled() &&
       (n - head) / (4 * tma_cfg().nt) >= 1) {
@@ -470,12 +498,13 @@ int dos_adam_launch(float* p, float* m, float* v, const void* g, int gt, void* l
     const char* gc = static_cast<const char*>(g);
     char* lc = static_cast<char*>(lp);
     int rc = DOS_OK;
-    if (head > 0) rc = dos_adam_launch(p, m, v, g, gt, lp, lt, head, s, st);  // < 8 elements: register path
+    if (head > 0) rc = dos_adam_launch(p, m, v, g, gt, lp, lt, head, s, st, pr);  // < 8 elements: register path
     if (rc != DOS_OK) return rc;
     const uint16_t* gb = reinterpret_cast<const uint16_t*>(gc + 2 * head);
     uint16_t* wb = lt == DOS_NONE ? nullptr : reinterpret_cast<uint16_t*>(lc + 2 * head);
+    const dos_peers pb = dos_peers_offset(pr, head);
 #define DOS_TMA(G, L) \
-  if (gt == G && lt == L) rc = launch_adam_tma<G, L>(p + head, m + head, v + head, gb, wb, ntiles, tail, s, st);
+  if (gt == G && lt == L) rc = launch_adam_tma<G, L>(p + head, m + head, v + head, gb, wb, ntiles, tail, s, st, pb);
     DOS_TMA(DOS_F16, DOS_NONE) else DOS_TMA(DOS_F16, DOS_F16) else DOS_TMA(DOS_F16, DOS_BF16)
     else DOS_TMA(DOS_BF16, DOS_NONE) else DOS_TMA(DOS_BF16, DOS_F16) else DOS_TMA(DOS_BF16, DOS_BF16)
 #undef DOS_TMA
@@ -491,7 +520,7 @@ int dos_adam_launch(float* p, float* m, float* v, const void* g, int gt, void* l
     nvec = (n - head) / kVec;
   }
 #define DOS_CASE(G, L) \
-  if (gt == G && lt == L) { launch_adam<G, L>(p, m, v, g, lp, head, nvec, n, s, st); }
+  if (gt == G && lt == L) { launch_adam<G, L>(p, m, v, g, lp, head, nvec, n, s, st, pr); }
   DOS_CASE(DOS_F32, DOS_NONE) else DOS_CASE(DOS_F32, DOS_F16) else DOS_CASE(DOS_F32, DOS_BF16)
   else DOS_CASE(DOS_F16, DOS_NONE) else DOS_CASE(DOS_F16, DOS_F16) else DOS_CASE(DOS_F16, DOS_BF16)
   else DOS_CASE(DOS_BF16, DOS_NONE) else DOS_CASE(DOS_BF16, DOS_F16) else DOS_CASE(DOS_BF16, DOS_BF16)
@@ -514,6 +543,28 @@ extern "C" int dos_adam_step_cuda(float* p, float* m, float* v, const void* g, i
     return dos_set_error(DOS_EINVAL, "NULL buffer");
   return dos_adam_launch(p, m, v, g, g_dtype, p_lowp, lowp_dtype, n, dos_make_kscal(s),
                          reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int dos_adam_step_cuda_bcast(float* p, float* m, float* v, const void* g, int g_dtype, void* p_lowp,
+                                        int lowp_dtype, void* const* peer_lowp, int npeers, int64_t n,
+                                        const dos_adam_scalars* s, void* stream) {
+  if (npeers < 0 || npeers > DOS_MAX_PEERS) return dos_set_error(DOS_EINVAL, "npeers must be in [0, %d]", DOS_MAX_PEERS);
+  if (npeers > 0 && (lowp_dtype == DOS_NONE || !peer_lowp)) return dos_set_error(DOS_EINVAL, "peers need a working copy");
+  if (!s) return dos_set_error(DOS_EINVAL, "scalars must not be NULL");
+  if (n < 0) return dos_set_error(DOS_EINVAL, "n must be >= 0");
+  if (g_dtype != DOS_F32 && g_dtype != DOS_F16 && g_dtype != DOS_BF16)
+    return dos_set_error(DOS_ETYPE, "grad dtype %d unsupported", g_dtype);
+  if (lowp_dtype != DOS_NONE && lowp_dtype != DOS_F16 && lowp_dtype != DOS_BF16)
+    return dos_set_error(DOS_ETYPE, "working-copy dtype %d unsupported", lowp_dtype);
+  if (n > 0 && (!p || !m || !v || !g || (lowp_dtype != DOS_NONE && !p_lowp)))
+    return dos_set_error(DOS_EINVAL, "NULL buffer");
+  dos_peers pr{npeers, {}};
+  for (int r = 0; r < npeers; ++r) {
+    if (!peer_lowp[r]) return dos_set_error(DOS_EINVAL, "NULL peer pointer %d", r);
+    pr.p[r] = static_cast<uint16_t*>(peer_lowp[r]);
+  }
+  return dos_adam_launch(p, m, v, g, g_dtype, p_lowp, lowp_dtype, n, dos_make_kscal(s),
+                         reinterpret_cast<cudaStream_t>(stream), pr);
 }
 
 extern "C" int dos_downscale_cuda(const float* x, void* out, int out_dtype, int64_t n, void* stream) {

@@ -77,6 +77,7 @@ struct Engine {
   dos_state_desc S{};
   std::vector<int64_t> sg_start, sg_size, static_off;
   dos_kscal K{};
+  dos_peers peers{0, {}};  // fused all-gather targets (shard element 0 in each peer)
   int32_t max_actions = 0, count = 0;
   std::vector<cudaEvent_t> ev_s, ev_e;
   cudaEvent_t ev0 = nullptr;
@@ -314,14 +315,15 @@ struct Engine {
           const int64_t o = static_off[sg];
           if (o < 0) return dos_set_error(DOS_ESTATE, "subgroup %d marked static but has no HBM residence", sg);
           if (S.host_io) DOS_CU(copy_grads_h2d(start, n, s));
-          return dos_adam_launch(S.dev_static_p + o, S.dev_static_m + o, S.dev_static_v + o, g, lt, lp, lt, n, K, s);
+          return dos_adam_launch(S.dev_static_p + o, S.dev_static_m + o, S.dev_static_v + o, g, lt, lp, lt, n, K, s,
+                                 dos_peers_offset(peers, start));
         }
         if (sg_slot[sg] < 0 || sg_mask[sg] != 7u)
           return dos_set_error(DOS_ESTATE, "fast update of subgroup %d with missing pieces (mask %u)", sg,
                                (unsigned)sg_mask[sg]);
         const int sl = sg_slot[sg];
         return dos_adam_launch(slot_ptr(sl, PIECE_P), slot_ptr(sl, PIECE_M), slot_ptr(sl, PIECE_V), g, lt, lp, lt, n,
-                               K, s);
+                               K, s, dos_peers_offset(peers, start));
       }
       case DOS_FLUSH_OUT_MODEL16:
         // K1 already stored the working copy in the same pass.
@@ -349,6 +351,9 @@ struct Engine {
       case DOS_H2D_PARAMS16:
         DOS_CU(cudaMemcpyAsync(dev_lowp + 2 * start, static_cast<const char*>(S.host_lowp) + 2 * start, (size_t)n * 2,
                                cudaMemcpyHostToDevice, s));
+        // fused all-gather for a host subgroup: forward it peer-to-peer (NVLink copy engine)
+        for (int r = 0; r < peers.n; ++r)
+          DOS_CU(cudaMemcpyAsync(peers.p[r] + start, dev_lowp + 2 * start, (size_t)n * 2, cudaMemcpyDeviceToDevice, s));
         return DOS_OK;
       default:
         return dos_set_error(DOS_EINVAL, "unexpected action kind %d on a device lane", a->kind);
@@ -369,6 +374,10 @@ struct Engine {
     if (S.static_offset) static_off.assign(S.static_offset, S.static_offset + ns);
     else static_off.assign(ns, -1);
     K = dos_make_kscal(sc);
+    if (S.npeers < 0 || S.npeers > DOS_MAX_PEERS || (S.npeers > 0 && !S.peer_lowp))
+      return dos_set_error(DOS_EINVAL, "npeers must be in [0, %d] with peer pointers", DOS_MAX_PEERS);
+    peers.n = S.npeers;
+    for (int r = 0; r < S.npeers; ++r) peers.p[r] = static_cast<uint16_t*>(S.peer_lowp[r]);
     const int32_t cap = nmax > 0 ? nmax : 1;
     while ((int32_t)ev_s.size() < cap) {
       cudaEvent_t a, b;

@@ -17,9 +17,17 @@ int dos_set_error(int code, const char* fmt, ...);
 // Per-launch scalars from the C-ABI struct (fp32 arithmetic on the host).
 dos_kscal dos_make_kscal(const dos_adam_scalars* s);
 
+// Peer destinations of the working copy (fused all-gather); element 0 of
+// each pointer corresponds to element 0 of the launch's range.
+struct dos_peers {
+  int n;
+  uint16_t* p[DOS_MAX_PEERS];
+};
+dos_peers dos_peers_offset(const dos_peers& pr, int64_t elems);
+
 // K1 launch without argument validation (used by the engine).
 int dos_adam_launch(float* p, float* m, float* v, const void* g, int gt, void* lp, int lt, int64_t n,
-                    const dos_kscal& s, cudaStream_t st);
+                    const dos_kscal& s, cudaStream_t st, const dos_peers& pr = dos_peers{0, {}});
 
 // Host kernels (dos_host.cpp); the calling thread joins the team.
 int dos_host_adam(float* p, float* m, float* v, const void* g, int gt, void* lp, int lt, int64_t n,

@@ -185,9 +185,15 @@ class DeviceResidency:
             self._engines[key] = eng
         return eng
 
-    def state_desc(self, host_io: bool = False) -> tuple[N.dos_state_desc, list]:
+    def state_desc(self, host_io: bool = False, peers=None) -> tuple[N.dos_state_desc, list]:
+        """``peers``: addresses (ints) where this shard starts in each peer's
+        full-model buffer — the fused all-gather targets (include/dos.h)."""
         opt = self.opt
-        keep = [self.sg_start, self.sg_size, self.static_off]
+        peers = list(peers or ())
+        if len(peers) > N.DOS_MAX_PEERS:
+            raise ValueError(f"at most {N.DOS_MAX_PEERS} peers")
+        peer_arr = (C.c_void_p * max(1, len(peers)))(*peers)
+        keep = [self.sg_start, self.sg_size, self.static_off, peer_arr]
         p64 = C.POINTER(C.c_int64)
         d = N.dos_state_desc(
             num_subgroups=len(opt.subgroups),
@@ -202,6 +208,8 @@ class DeviceResidency:
             dev_static_m=self.static_m.data_ptr() if self.static_m is not None else None,
             dev_static_v=self.static_v.data_ptr() if self.static_v is not None else None,
             host_io=1 if host_io else 0,
+            npeers=len(peers),
+            peer_lowp=C.cast(peer_arr, C.POINTER(C.c_void_p)),
         )
         return d, keep
 
@@ -293,7 +301,7 @@ class B200Target(SimTarget):
 
     def __init__(self, profile: SystemProfile, plan: UpdatePlan, optimizer: ShardedOptimizer, hyper,
                  step: int, *, host_threads: int = 0, fuse_downscale: bool = True,
-                 host_io: bool = False) -> None:
+                 host_io: bool = False, peers=None) -> None:
         sizes = tuple(g.size for g in optimizer.subgroups)
         super().__init__(profile, plan, sizes)
         self.opt = optimizer
@@ -305,11 +313,12 @@ class B200Target(SimTarget):
         self.engine = self.residency.engine(self.num_slots, slot_elems, host_threads, fuse_downscale)
         self._descs = plan_descs(plan)
         self.host_io = host_io
+        self.peers = list(peers or ())
         self._begun = False
         self._submitted = 0
 
     def _begin(self) -> None:
-        desc, keep = self.residency.state_desc(self.host_io)
+        desc, keep = self.residency.state_desc(self.host_io, self.peers)
         self._keep = (desc, keep)
         h = self.hyper
         bc1, bc2 = bias_corrections(h.beta1, h.beta2, self.step)

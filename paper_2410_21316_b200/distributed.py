@@ -150,6 +150,54 @@ class BucketedCollectives:
                 w.wait()
 
 
+class PeerTargets:
+    """The fused all-gather's destinations: every peer's full-model buffer,
+    mapped into this process with CUDA IPC (one node, NVLink/NVSwitch P2P).
+
+    ``targets`` lists, for each other rank, the address where *this* rank's
+    shard begins inside that rank's full-model buffer; passed as
+    ``execute_plan(..., peers=targets)``, K1 stores every updated working-copy
+    element there in the same pass (and the copy engine forwards host
+    subgroups after their H2D_PARAMS16), so no separate all-gather runs.
+    Callers synchronise the ranks (a barrier) after the phase before
+    reading the gathered buffer.
+    """
+
+    def __init__(self, full_params, layout: ShardLayout, group=None) -> None:
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        from . import _native as N
+
+        if full_params.element_size() != 2:
+            raise TypeError("the full-model buffer must be half precision")
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        if world - 1 > N.DOS_MAX_PEERS:
+            raise ValueError(f"fused all-gather supports up to {N.DOS_MAX_PEERS + 1} ranks")
+        handle = C.create_string_buffer(64)
+        off = C.c_uint64()
+        N.check(N.lib().dos_ipc_export(full_params.data_ptr(), handle, C.byref(off)))
+        mine = (rank, handle.raw, off.value)
+        everyone = [None] * world
+        dist.all_gather_object(everyone, mine, group=group)
+        self.bases: dict[int, int] = {}
+        for r, h, o in everyone:
+            if r == rank:
+                continue
+            ptr = C.c_void_p()
+            N.check(N.lib().dos_ipc_import(h, o, C.byref(ptr)))
+            self.bases[r] = ptr.value
+        shard_bytes = 2 * rank * layout.per_rank
+        self.targets = [self.bases[r] + shard_bytes for r in sorted(self.bases)]
+        self.group = group
+
+    def barrier(self) -> None:
+        import torch.distributed as dist
+
+        dist.barrier(group=self.group)
+
+
 def gather_params_overlapped(coll: BucketedCollectives, plan, working_copy, full_params, comm_stream=None):
     """``execute_plan(..., on_submitted=...)`` hook: all-gather each bucket as
     soon as this rank's subgroup j has its final working copy.

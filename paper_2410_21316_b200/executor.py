@@ -172,6 +172,7 @@ def execute_plan(
     check_coherence: bool = False,
     validate_measured: bool = True,
     on_submitted=None,
+    peers=None,
 ) -> ExecutionResult:
     """Run one optimizer step of ``plan`` on the B200; mutates ``optimizer``.
 
@@ -192,7 +193,8 @@ def execute_plan(
     if mode is ExecMode.THROTTLED and throttle_scale <= 0:
         raise ValueError("throttle_scale must be positive")
     step = optimizer.step + 1
-    target = B200Target(profile, plan, optimizer, hyper, step, host_threads=host_threads, host_io=host_io)
+    target = B200Target(profile, plan, optimizer, hyper, step, host_threads=host_threads, host_io=host_io,
+                        peers=peers)
     try:
         events = run_update(plan, target)
         if on_submitted is not None:  # e.g. chain per-subgroup collectives onto engine events

@@ -16,9 +16,13 @@ and ``step()`` runs
 1. a bucketed reduce-scatter of the bf16 grads into this rank's chunk
    (summed; ``average_grads`` divides by N),
 2. the D2H flush of the grads the host lane will read (§8(f) row 1),
-3. the update phase (``execute_plan``), with every bucket's all-gather of
-   the working copy chained onto the engine event that finalises its
-   subgroup (``distributed.gather_params_overlapped``),
+3. the update phase (``execute_plan``) with the all-gather fused in: K1
+   stores every updated working-copy element into each peer's full-model
+   buffer over NVLink (CUDA IPC, ``distributed.PeerTargets``) and the copy
+   engine forwards host subgroups after their H2D_PARAMS16, then one
+   barrier; with ``fused_gather=False`` each bucket's NCCL all-gather is
+   instead chained onto the engine event that finalises its subgroup
+   (``distributed.gather_params_overlapped``),
 4. a per-iteration re-fit: explore-then-exploit over strides by measured
    span (``policy.StrideTuner``), identical on every rank.
 """
@@ -28,7 +32,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import policy
-from .distributed import BucketedCollectives, ShardLayout, gather_params_overlapped
+from .distributed import BucketedCollectives, PeerTargets, ShardLayout, gather_params_overlapped
 from .executor import AdamHyper, execute_plan
 from .plan import Device, build_plan
 from .state import ShardedOptimizer, lowp_downscale
@@ -37,7 +41,8 @@ from .state import ShardedOptimizer, lowp_downscale
 class DeepOptimizerStates:
     def __init__(self, params, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 0.0,
                  *, subgroup_size: int = 100_000_000, profile=None, stride="auto", static_ratio: float = 0.0,
-                 master_params=None, process_group=None, average_grads: bool = False, explore: int = 3) -> None:
+                 master_params=None, process_group=None, average_grads: bool = False, explore: int = 3,
+                 fused_gather: bool = True) -> None:
         import torch
         import torch.distributed as dist
 
@@ -90,6 +95,9 @@ class DeepOptimizerStates:
         self.opt = opt
         self.res = opt.to_device(dev, grads=self.flat_grad[self.offset:self.offset + mine], model16=chunk)
         self.coll = BucketedCollectives(lay, process_group) if self.world > 1 else None
+        # fused all-gather: K1 writes the working copy straight into every
+        # peer's full-model buffer (IPC-mapped); else bucketed overlapped gathers
+        self.peers = PeerTargets(self.flat, lay, process_group) if (self.world > 1 and fused_gather) else None
 
         if profile is None:
             from .catalog import get_profile
@@ -154,14 +162,18 @@ class DeepOptimizerStates:
             self._reduce_grads()
             torch.cuda.current_stream(self.res.device).synchronize()
         self._flush_host_grads()
-        hook = gather_params_overlapped(self.coll, self.plan, self.res.model16, self.flat) \
-            if self.coll is not None else None
-        self.last = execute_plan(self.opt, self.plan, self.profile, self.hyper, on_submitted=hook)
+        hook = None
+        if self.coll is not None and self.peers is None:
+            hook = gather_params_overlapped(self.coll, self.plan, self.res.model16, self.flat)
+        self.last = execute_plan(self.opt, self.plan, self.profile, self.hyper, on_submitted=hook,
+                                 peers=self.peers.targets if self.peers is not None else None)
         if hook is not None:
             for w in hook.works:
                 if w is not None:
                     w.wait()
             torch.cuda.current_stream(self.res.device).wait_stream(hook.stream)
+        if self.peers is not None:
+            self.peers.barrier()  # every rank's peer stores have landed (each finished its phase)
         if self.tuner is not None and self.last.measured is not None:
             self.tuner.record(self.plan.stride, int(self._max_over_ranks(self.last.measured.span_ns)))
             nxt = self.tuner.next_stride()

@@ -130,3 +130,37 @@ def test_device_conversions_exact():
         ref = O.f32_from_lowp(allb.cpu().numpy().view(np.uint16).view(np.float16) if kind == "fp16"
                               else allb.cpu().numpy().view(np.uint16), kind)
         assert up.cpu().numpy().view(np.uint32).tobytes() == ref.view(np.uint32).tobytes()
+
+
+@pytest.mark.parametrize("npeers", [1, 3, 7])
+@pytest.mark.parametrize("n,off", [(5, 0), (4096 * 3 + 77, 0), (1_000_003, 3)])
+def test_k1_fused_broadcast_to_peers(npeers, n, off):
+    """dos_adam_step_cuda_bcast: every peer destination receives exactly the
+    local working copy (local buffers stand in for IPC-mapped peers)."""
+    p, m, v, g32 = _inputs(n, 11 + n)
+    g = O.bf16_from_f32(g32)
+    rp, rm, rv = p.copy(), m.copy(), v.copy()
+    O.adam_step(rp, rm, rv, O.f32_from_bf16(g), 1e-3, 0.9, 0.999, 1e-8, 2)
+    dev = torch.device("cuda")
+    pad = 8
+    tp, tm, tv = (torch.zeros(n + pad, dtype=torch.float32, device=dev) for _ in range(3))
+    tg = torch.zeros(n + pad, dtype=torch.int16, device=dev)
+    tw = torch.zeros(n + pad, dtype=torch.int16, device=dev)
+    peers = [torch.zeros(n + pad, dtype=torch.int16, device=dev) for _ in range(npeers)]
+    for t, x in ((tp, p), (tm, m), (tv, v)):
+        t[off:off + n] = torch.from_numpy(x)
+    tg[off:off + n] = torch.from_numpy(g.view(np.int16))
+    import ctypes as C
+
+    arr = (C.c_void_p * npeers)(*[q.data_ptr() + 2 * off for q in peers])
+    sc = N.scalars(1e-3, 0.9, 0.999, 1e-8, *O.bias_corrections(0.9, 0.999, 2))
+    N.check(N.lib().dos_adam_step_cuda_bcast(tp.data_ptr() + 4 * off, tm.data_ptr() + 4 * off, tv.data_ptr() + 4 * off,
+                                             tg.data_ptr() + 2 * off, N.DOS_BF16, tw.data_ptr() + 2 * off, N.DOS_BF16,
+                                             arr, npeers, n, sc, None))
+    torch.cuda.synchronize()
+    want = O.bf16_from_f32(rp).tobytes()
+    assert tp[off:off + n].cpu().numpy().tobytes() == rp.tobytes()
+    assert tw[off:off + n].cpu().numpy().view(np.uint16).tobytes() == want
+    for q in peers:
+        assert q[off:off + n].cpu().numpy().view(np.uint16).tobytes() == want
+        assert torch.count_nonzero(q[:off]) == 0 and torch.count_nonzero(q[off + n:]) == 0

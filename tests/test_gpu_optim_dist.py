@@ -23,7 +23,7 @@ def _port() -> int:
     return p
 
 
-def _worker(rank, world, port, stride, q):
+def _worker(rank, world, port, stride, fused, q):
     try:
         import torch.distributed as dist
 
@@ -39,7 +39,8 @@ def _worker(rank, world, port, stride, q):
             torch.bfloat16)
         init = torch.cat([p.detach().reshape(-1) for p in model.parameters()]).float().cpu().numpy().copy()
         opt = DeepOptimizerStates(model.parameters(), lr=1e-3, subgroup_size=9_000, profile=get_profile("h100-node"),
-                                  stride=stride, static_ratio=0.2, process_group=dist.group.WORLD)
+                                  stride=stride, static_ratio=0.2, process_group=dist.group.WORLD,
+                                  fused_gather=fused)
         lay, off = opt.layout, opt.offset
         mine = opt.opt.total_params
         st = {"p": init[off:off + mine].copy(), "m": np.zeros(mine, np.float32), "v": np.zeros(mine, np.float32),
@@ -68,14 +69,14 @@ def _worker(rank, world, port, stride, q):
         q.put((rank, False, traceback.format_exc()))
 
 
-@pytest.mark.parametrize("stride", [2, "auto"])
-def test_two_rank_zero3_step_matches_oracle(stride):
+@pytest.mark.parametrize("stride,fused", [(2, False), ("auto", False), (2, True), ("auto", True)])
+def test_two_rank_zero3_step_matches_oracle(stride, fused):
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, stride, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, stride, fused, q)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in procs]
