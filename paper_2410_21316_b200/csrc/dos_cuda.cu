@@ -250,8 +250,8 @@ void launch_adam(float* p, float* m, float* v, const void* g, void* lp, int64_t 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+__device__ __forceinline__ void mbar_init1(uint64_t* bar) {  // expected arrivals: one (the producer)
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(NT, 1)
   };
 
   if (tid == 0) {
-    for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i < S; ++i) mbar_init1(&full[i]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");  // inits visible to the async proxy
     fence_async_smem();
   }
