@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--host-threads", type=int, default=0, help="H1 team size (0: all allowed cores / ranks)")
     ap.add_argument("--trace-dir", default=None, help="write measured/predicted timelines as trace CSVs")
+    ap.add_argument("--no-ref-schedule", action="store_true",
+                    help="skip timing the reference's ALL_CPU offload schedule on this runtime")
     ap.add_argument("--static-variants", default="0.0,0.5,1.0",
                     help="extra measured runs with HBM-resident static subgroups ('' to skip)")
     ap.add_argument("--profile-out", default=None)
@@ -503,6 +505,26 @@ def main() -> None:
         vms = max_over_ranks(g0.elapsed_time(g1) / args.steps)
         variants.append({"static_ratio": ratio, "stride": vstride, "ms_per_step": vms, "value": P / (vms * 1e-3),
                          "hbm_resident_state_bytes": 12 * sum(sizes[i] for i in vplan.static_set) * world})
+    # the reference's own offload-to-CPU schedule (ALL_CPU blocking plan,
+    # scheduler.py:301-319: update, downscale, H2D of the half-precision
+    # params, serialised per subgroup) executed by this runtime on the same
+    # box — the denominator of the north star's ">= 2x lower update time"
+    ref_sched = None
+    if not args.no_ref_schedule:
+        rplan = D.build_plan(nsg, D.ALL_CPU)
+        D.execute_plan(opt, rplan, profile, hyper)
+        barrier()
+        torch.cuda.synchronize()
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record()
+        for _ in range(2):
+            D.execute_plan(opt, rplan, profile, hyper)
+        h1.record()
+        torch.cuda.synchronize()
+        rms = max_over_ranks(h0.elapsed_time(h1) / 2)
+        ref_sched = {"ms_per_step": rms, "value": P / (rms * 1e-3),
+                     "speedup_of_headline": rms / ms_max,
+                     "plan": "build_plan(N, ALL_CPU): CPU_UPDATE -> CPU_DOWNSCALE -> H2D_PARAMS16 chained"}
     if variants:
         opt.residency.set_static(plan.static_set)  # back to the headline placement
         torch.cuda.empty_cache()
@@ -582,6 +604,7 @@ def main() -> None:
                         "host_threads": D._native.lib().dos_host_threads()},
             "setup_s": {"alloc_pin": t_alloc, "fill": t_fill},
             "static_variants": variants,
+            "reference_offload_schedule": ref_sched,
             "collectives": collectives,
         }
         print(json.dumps(line), flush=True)
