@@ -457,19 +457,24 @@ def main() -> None:
         torch.cuda.synchronize()
         phase_ag_ms = max_over_ranks((time.perf_counter() - t0) * 1e3)
         # fused: K1 stores the working copy into every peer's full buffer (IPC / NVLink)
-        fused_ms = None
+        fused_ms, peers, why = None, None, ""
         try:
             from paper_2410_21316_b200.distributed import PeerTargets
 
             peers = PeerTargets(full, lay)
+        except Exception as exc:  # e.g. no P2P between these GPUs
+            why = str(exc)[:160]
+        # every rank must agree before anyone waits in the fused phase's barrier
+        all_ok = -max_over_ranks(-1.0 if peers is not None else 0.0) >= 1.0
+        if all_ok:
             barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             D.execute_plan(opt, plan, profile, hyper, peers=peers.targets)
             peers.barrier()
             fused_ms = max_over_ranks((time.perf_counter() - t0) * 1e3)
-        except Exception as exc:  # e.g. no P2P between these GPUs: report, keep the NCCL numbers
-            fused_ms = f"unavailable: {exc}"[:200]
+        else:
+            fused_ms = f"unavailable: {why or 'a peer could not map the IPC buffers'}"
         collectives = {"reduce_scatter_ms": rs_ms, "all_gather_ms": ag_ms, "buckets": lay.num_buckets,
                        "bytes_per_rank_each": 2 * lay.padded_total,
                        "phase_with_overlapped_all_gather_ms": phase_ag_ms,
