@@ -163,6 +163,11 @@ typedef struct dos_state_desc {
    * by the copy engine right after its H2D_PARAMS16.  npeers <= DOS_MAX_PEERS. */
   int32_t npeers;
   void* const* peer_lowp;
+  /* flush_grads != 0: the gradient flush of SURVEY §8(f) row 1 runs inside
+   * the phase — each CPU_UPDATE's bf16/fp16 grads are copied dev_g -> host_g
+   * (pinned DMA, in subgroup order, on a dedicated stream) and the host lane
+   * waits only for its own subgroup's copy; the upcast is fused into H1. */
+  int32_t flush_grads;
 } dos_state_desc;
 
 #define DOS_MAX_PEERS 7

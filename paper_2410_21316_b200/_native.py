@@ -57,6 +57,7 @@ class dos_state_desc(C.Structure):
         ("host_io", C.c_int32),
         ("npeers", C.c_int32),
         ("peer_lowp", C.POINTER(C.c_void_p)),
+        ("flush_grads", C.c_int32),
     ]
 
 

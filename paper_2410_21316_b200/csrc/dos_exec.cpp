@@ -61,11 +61,14 @@ enum { PIECE_M = 0, PIECE_V = 1, PIECE_P = 2 };
 struct Job {
   int32_t id, kind, sg;
   std::vector<int32_t> deps, batch;
+  cudaEvent_t flushed = nullptr;  // in-phase grad flush of this subgroup (flush_grads)
 };
 
 struct Engine {
   int dev = 0;
   cudaStream_t st[3] = {nullptr, nullptr, nullptr};  // fast, h2d, d2h
+  cudaStream_t gst = nullptr;                        // in-phase grad flush (D2H)
+  std::vector<cudaEvent_t> ev_g;                      // per action: its grads are on the host
   int nslots = 0;
   int64_t slot_elems = 0;
   float* slot_mem = nullptr;
@@ -144,6 +147,13 @@ struct Engine {
             rc = DOS_ECUDA;
             msg = std::string("waiting on GPU dep failed: ") + cudaGetErrorString(e);
           }
+        }
+      }
+      if (j.flushed) {  // this subgroup's grads reached the host image
+        cudaError_t e = cudaEventSynchronize(j.flushed);
+        if (e != cudaSuccess && rc == DOS_OK) {
+          rc = DOS_ECUDA;
+          msg = std::string("waiting on the grad flush failed: ") + cudaGetErrorString(e);
         }
       }
       const int64_t t_s = now_ns();
@@ -239,6 +249,16 @@ struct Engine {
       j.batch.assign(a->batch, a->batch + a->batch_len);
       for (int32_t b : j.batch)
         if (b < 0 || b >= S.num_subgroups) return fail(DOS_EINVAL, "downscale batch names a bad subgroup");
+      if (S.flush_grads && a->kind == DOS_CPU_UPDATE) {
+        // §8(f) row 1 inside the phase: this subgroup's half-precision grads
+        // D2H on their own stream, in emission (= subgroup) order
+        const int64_t start = sg_start[sg], n = sg_size[sg];
+        DOS_CU(cudaMemcpyAsync(static_cast<char*>(const_cast<void*>(S.host_g)) + 2 * start,
+                               static_cast<const char*>(S.dev_g) + 2 * start, (size_t)n * 2, cudaMemcpyDeviceToHost,
+                               gst));
+        DOS_CU(cudaEventRecord(ev_g[a->id], gst));
+        j.flushed = ev_g[a->id];
+      }
       {
         std::lock_guard<std::mutex> lk(mu);
         q.push_back(std::move(j));
@@ -380,11 +400,13 @@ struct Engine {
     for (int r = 0; r < S.npeers; ++r) peers.p[r] = static_cast<uint16_t*>(S.peer_lowp[r]);
     const int32_t cap = nmax > 0 ? nmax : 1;
     while ((int32_t)ev_s.size() < cap) {
-      cudaEvent_t a, b;
+      cudaEvent_t a, b, c;
       DOS_CU(cudaEventCreate(&a));
       DOS_CU(cudaEventCreate(&b));
+      DOS_CU(cudaEventCreateWithFlags(&c, cudaEventDisableTiming));
       ev_s.push_back(a);
       ev_e.push_back(b);
+      ev_g.push_back(c);
     }
     if (flags_cap < cap) {
       if (flags) cudaFreeHost(flags);
@@ -421,6 +443,7 @@ struct Engine {
     DOS_CU(cudaEventRecord(ev0, st[0]));
     DOS_CU(cudaStreamWaitEvent(st[1], ev0, 0));
     DOS_CU(cudaStreamWaitEvent(st[2], ev0, 0));
+    DOS_CU(cudaStreamWaitEvent(gst, ev0, 0));
     DOS_CU(cudaEventSynchronize(ev0));
     host_t0 = now_ns();
     active = true;
@@ -435,8 +458,8 @@ struct Engine {
     }
     active = false;
     cudaError_t ce = cudaSuccess;
-    for (int i = 0; i < 3; ++i) {
-      cudaError_t e = cudaStreamSynchronize(st[i]);
+    for (int i = 0; i < 4; ++i) {
+      cudaError_t e = cudaStreamSynchronize(i < 3 ? st[i] : gst);
       if (e != cudaSuccess && ce == cudaSuccess) ce = e;
     }
     if (ce != cudaSuccess) return dos_set_error(DOS_ECUDA, "update phase failed on the device: %s", cudaGetErrorString(ce));
@@ -471,6 +494,7 @@ struct Engine {
     if (slot_elems < 0) return dos_set_error(DOS_EINVAL, "slot_elems must be >= 0");
     DOS_CU(cudaSetDevice(dev));
     for (int i = 0; i < 3; ++i) DOS_CU(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking));
+    DOS_CU(cudaStreamCreateWithFlags(&gst, cudaStreamNonBlocking));
     DOS_CU(cudaEventCreate(&ev0));
     if (slot_elems > 0) DOS_CU(cudaMalloc(reinterpret_cast<void**>(&slot_mem), (size_t)nslots * 3 * slot_elems * 4));
     cudaDriverEntryPointQueryResult qr;
@@ -497,8 +521,13 @@ struct Engine {
         cudaStreamSynchronize(st[i]);
         cudaStreamDestroy(st[i]);
       }
+    if (gst) {
+      cudaStreamSynchronize(gst);
+      cudaStreamDestroy(gst);
+    }
     for (auto e : ev_s) cudaEventDestroy(e);
     for (auto e : ev_e) cudaEventDestroy(e);
+    for (auto e : ev_g) cudaEventDestroy(e);
     if (ev0) cudaEventDestroy(ev0);
     if (slot_mem) cudaFree(slot_mem);
     if (flags) cudaFreeHost(flags);

@@ -185,7 +185,7 @@ class DeviceResidency:
             self._engines[key] = eng
         return eng
 
-    def state_desc(self, host_io: bool = False, peers=None) -> tuple[N.dos_state_desc, list]:
+    def state_desc(self, host_io: bool = False, peers=None, flush_grads: bool = False) -> tuple[N.dos_state_desc, list]:
         """``peers``: addresses (ints) where this shard starts in each peer's
         full-model buffer — the fused all-gather targets (include/dos.h)."""
         opt = self.opt
@@ -210,6 +210,7 @@ class DeviceResidency:
             host_io=1 if host_io else 0,
             npeers=len(peers),
             peer_lowp=C.cast(peer_arr, C.POINTER(C.c_void_p)),
+            flush_grads=1 if flush_grads else 0,
         )
         return d, keep
 
@@ -301,7 +302,9 @@ class B200Target(SimTarget):
 
     def __init__(self, profile: SystemProfile, plan: UpdatePlan, optimizer: ShardedOptimizer, hyper,
                  step: int, *, host_threads: int = 0, fuse_downscale: bool = True,
-                 host_io: bool = False, peers=None) -> None:
+                 host_io: bool = False, peers=None, flush_grads: bool = False) -> None:
+        if host_io and flush_grads:
+            raise ValueError("host_io reads the grads from the host image; flush_grads copies them there")
         sizes = tuple(g.size for g in optimizer.subgroups)
         super().__init__(profile, plan, sizes)
         self.opt = optimizer
@@ -314,11 +317,12 @@ class B200Target(SimTarget):
         self._descs = plan_descs(plan)
         self.host_io = host_io
         self.peers = list(peers or ())
+        self.flush_grads = flush_grads
         self._begun = False
         self._submitted = 0
 
     def _begin(self) -> None:
-        desc, keep = self.residency.state_desc(self.host_io, self.peers)
+        desc, keep = self.residency.state_desc(self.host_io, self.peers, self.flush_grads)
         self._keep = (desc, keep)
         h = self.hyper
         bc1, bc2 = bias_corrections(h.beta1, h.beta2, self.step)

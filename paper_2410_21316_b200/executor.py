@@ -173,6 +173,7 @@ def execute_plan(
     validate_measured: bool = True,
     on_submitted=None,
     peers=None,
+    flush_grads: bool = False,
 ) -> ExecutionResult:
     """Run one optimizer step of ``plan`` on the B200; mutates ``optimizer``.
 
@@ -187,6 +188,13 @@ def execute_plan(
     ship theirs H2D inside their prefetch — and the working copy is mirrored
     into the host ``model16`` inside the flushes, so both host images are
     coherent when the call returns.
+
+    ``flush_grads=True`` moves the gradient flush into
+    the phase: the device grads of each host-updated subgroup are copied D2H
+    on their own stream in subgroup order and each CPU_UPDATE waits only for
+    its own subgroup (the upcast stays fused in H1).  ``peers`` enables the
+    fused all-gather (``distributed.PeerTargets``); ``on_submitted(target)``
+    runs after the last submit, before the wait.
     """
     if plan.num_subgroups != len(optimizer.subgroups):
         raise ValueError(f"plan covers {plan.num_subgroups} subgroups, optimizer has {len(optimizer.subgroups)}")
@@ -194,7 +202,7 @@ def execute_plan(
         raise ValueError("throttle_scale must be positive")
     step = optimizer.step + 1
     target = B200Target(profile, plan, optimizer, hyper, step, host_threads=host_threads, host_io=host_io,
-                        peers=peers)
+                        peers=peers, flush_grads=flush_grads)
     try:
         events = run_update(plan, target)
         if on_submitted is not None:  # e.g. chain per-subgroup collectives onto engine events

@@ -15,7 +15,8 @@ and ``step()`` runs
 
 1. a bucketed reduce-scatter of the bf16 grads into this rank's chunk
    (summed; ``average_grads`` divides by N),
-2. the D2H flush of the grads the host lane will read (§8(f) row 1),
+2. inside the phase, the D2H flush of the grads the host lane will read
+   (§8(f) row 1; ``execute_plan(flush_grads=True)``),
 3. the update phase (``execute_plan``) with the all-gather fused in: K1
    stores every updated working-copy element into each peer's full-model
    buffer over NVLink (CUDA IPC, ``distributed.PeerTargets``) and the copy
@@ -161,12 +162,12 @@ class DeepOptimizerStates:
         if self.coll is not None:
             self._reduce_grads()
             torch.cuda.current_stream(self.res.device).synchronize()
-        self._flush_host_grads()
         hook = None
         if self.coll is not None and self.peers is None:
             hook = gather_params_overlapped(self.coll, self.plan, self.res.model16, self.flat)
+        # the host lane's grads are flushed D2H inside the phase (flush_grads)
         self.last = execute_plan(self.opt, self.plan, self.profile, self.hyper, on_submitted=hook,
-                                 peers=self.peers.targets if self.peers is not None else None)
+                                 peers=self.peers.targets if self.peers is not None else None, flush_grads=True)
         if hook is not None:
             for w in hook.works:
                 if w is not None:

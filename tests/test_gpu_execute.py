@@ -237,3 +237,25 @@ def test_baseline_config_shapes(name, nsub, tail):
         opt = D.ShardedOptimizer.initialize(total, sg, seed=nsub, lowp="bf16")
         D.execute_plan(opt, D.build_plan(nsub, k, static_ratio=ratio), prof, HYPER)
         assert digest(opt) == oracle_digest(total, sg, nsub, "bf16"), (name, ratio, k)
+
+
+@pytest.mark.parametrize("stride,ratio", [(2, 0.0), (3, 0.25), (D.ALL_CPU, 0.0), (1, 0.0)])
+def test_in_phase_grad_flush(h100, stride, ratio):
+    """flush_grads=True: the device grads are the only source; the host lane
+    reads each subgroup's grads after its own in-phase D2H copy."""
+    opt = D.ShardedOptimizer.initialize(60_000, 6_000, seed=21, lowp="bf16")
+    want_g = opt.grads16.copy()
+    res = opt.to_device()
+    opt._g[:] = 0x7FC0  # poison the host image: only the in-phase flush can repair it
+    plan = D.build_plan(10, stride, ratio)
+    D.execute_plan(opt, plan, h100, HYPER, flush_grads=True)
+    cpu = [sg for i, sg in enumerate(opt.subgroups) if plan.devices[i] is D.Device.CPU]
+    for sg in cpu:
+        assert opt.grads16[sg.slice].tobytes() == want_g[sg.slice].tobytes()
+    ref = O.initialize(60_000, 6_000, 21, "bf16")
+    O.sequential_oracle(ref)
+    assert opt.params32.tobytes() == ref["p"].tobytes()
+    assert opt.model16.tobytes() == ref["w"].tobytes()
+    with pytest.raises(ValueError):
+        D.execute_plan(opt, plan, h100, HYPER, flush_grads=True, host_io=True)
+    assert res is opt.residency
