@@ -278,6 +278,25 @@ __device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t 
                "r"(bytes)
                : "memory");
 }
+// Streaming variants: the state passes through L2 exactly once, so mark it
+// evict-first and leave L2 to the copy engines' traffic of the same phase.
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_load_ef(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store_ef(void* dst, const void* src, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -290,7 +309,7 @@ template <int GT, int LT, int NT, int S>
 __global__ void __launch_bounds__(NT, 1)
     k_adam_tma(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
                const uint16_t* __restrict__ g, uint16_t* __restrict__ w, int64_t ntiles, int64_t tail,
-               dos_kscal s, dos_peers pr) {
+               dos_kscal s, dos_peers pr, int l2ef) {
   constexpr int TE = 4 * NT;  // 4 elements per thread per tile
   constexpr uint32_t F32B = TE * 4, H16B = TE * 2, STAGE = 3 * F32B + H16B;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -298,16 +317,25 @@ __global__ void __launch_bounds__(NT, 1)
   const int tid = threadIdx.x;
   const int64_t first = blockIdx.x, step = gridDim.x;
   const int64_t mine = ntiles > first ? (ntiles - first + step - 1) / step : 0;
+  const uint64_t pol = l2ef ? l2_evict_first() : 0;
 
   auto stage_ptr = [&](int st, int piece) -> unsigned char* { return smem + st * STAGE + piece * F32B; };
+  auto load = [&](void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    if (l2ef) bulk_load_ef(dst, src, bytes, bar, pol);
+    else bulk_load(dst, src, bytes, bar);
+  };
+  auto store = [&](void* dst, const void* src, uint32_t bytes) {
+    if (l2ef) bulk_store_ef(dst, src, bytes, pol);
+    else bulk_store(dst, src, bytes);
+  };
   auto issue = [&](int64_t k) {  // tile k of this CTA into stage k % S
     const int st = (int)(k % S);
     const int64_t e0 = (first + k * step) * TE;
     mbar_expect_tx(&full[st], STAGE);
-    bulk_load(stage_ptr(st, 0), p + e0, F32B, &full[st]);
-    bulk_load(stage_ptr(st, 1), m + e0, F32B, &full[st]);
-    bulk_load(stage_ptr(st, 2), v + e0, F32B, &full[st]);
-    bulk_load(stage_ptr(st, 3), g + e0, H16B, &full[st]);
+    load(stage_ptr(st, 0), p + e0, F32B, &full[st]);
+    load(stage_ptr(st, 1), m + e0, F32B, &full[st]);
+    load(stage_ptr(st, 2), v + e0, F32B, &full[st]);
+    load(stage_ptr(st, 3), g + e0, H16B, &full[st]);
   };
 
   if (tid == 0) {
@@ -352,10 +380,10 @@ __global__ void __launch_bounds__(NT, 1)
     __syncthreads();
     if (tid == 0) {
       const int64_t e0 = (first + k * step) * TE;
-      bulk_store(p + e0, stage_ptr(st, 0), F32B);
-      bulk_store(m + e0, stage_ptr(st, 1), F32B);
-      bulk_store(v + e0, stage_ptr(st, 2), F32B);
-      if (LT != DOS_NONE) bulk_store(w + e0, stage_ptr(st, 3), H16B);
+      store(p + e0, stage_ptr(st, 0), F32B);
+      store(m + e0, stage_ptr(st, 1), F32B);
+      store(v + e0, stage_ptr(st, 2), F32B);
+      if (LT != DOS_NONE) store(w + e0, stage_ptr(st, 3), H16B);
       bulk_commit();
       if (k + S - 1 < mine) {
         bulk_wait_read<1>();  // the refilled stage's stores (tile k-1) have left shared memory
@@ -398,7 +426,13 @@ int launch_tma_cfg(float* p, float* m, float* v, const uint16_t* g, uint16_t* w,
   }
   const int64_t cap = (int64_t)sm_count() * ctas_per_sm;
   const int64_t grid = ntiles < cap ? ntiles : cap;
-  k_adam_tma<GT, LT, NT, S><<<(unsigned)grid, NT, smem, st>>>(p, m, v, g, w, ntiles, tail, s, pr);
+  // DOS_K1_L2=evict_first turns on L2 evict-first hints for the bulk copies;
+  // measured on the B200 they do not help (alone or under duplex DMA), so off.
+  static const int l2ef = [] {
+    const char* e = getenv("DOS_K1_L2");
+    return (e && strcmp(e, "evict_first") == 0) ? 1 : 0;
+  }();
+  k_adam_tma<GT, LT, NT, S><<<(unsigned)grid, NT, smem, st>>>(p, m, v, g, w, ntiles, tail, s, pr, l2ef);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return DOS_OK;
 }
