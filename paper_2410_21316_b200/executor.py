@@ -174,6 +174,7 @@ def execute_plan(
     on_submitted=None,
     peers=None,
     flush_grads: bool = False,
+    fuse_downscale: bool = True,
 ) -> ExecutionResult:
     """Run one optimizer step of ``plan`` on the B200; mutates ``optimizer``.
 
@@ -202,7 +203,7 @@ def execute_plan(
         raise ValueError("throttle_scale must be positive")
     step = optimizer.step + 1
     target = B200Target(profile, plan, optimizer, hyper, step, host_threads=host_threads, host_io=host_io,
-                        peers=peers, flush_grads=flush_grads)
+                        peers=peers, flush_grads=flush_grads, fuse_downscale=fuse_downscale)
     try:
         events = run_update(plan, target)
         if on_submitted is not None:  # e.g. chain per-subgroup collectives onto engine events

@@ -259,3 +259,12 @@ def test_in_phase_grad_flush(h100, stride, ratio):
     with pytest.raises(ValueError):
         D.execute_plan(opt, plan, h100, HYPER, flush_grads=True, host_io=True)
     assert res is opt.residency
+
+
+@pytest.mark.parametrize("stride", [2, 3, D.ALL_CPU])
+def test_unfused_cpu_downscale_matches(h100, stride):
+    """fuse_downscale=False: CPU_DOWNSCALE does its own pass over each batch
+    (the reference's separate action, executor.py:228-231)."""
+    opt = D.ShardedOptimizer.initialize(50_000, 5_000, seed=31, lowp="fp16")
+    D.execute_plan(opt, D.build_plan(10, stride, 0.2), h100, HYPER, fuse_downscale=False)
+    assert digest(opt) == oracle_digest(50_000, 5_000, 31)
