@@ -177,8 +177,8 @@ def run_reference(args, rank: int, world: int) -> None:
     # one step = the whole phase's work (P/SG subgroup passes, each over a
     # resident 1e8-param buffer far larger than the LLC)
     nsub = max(1, math.ceil(args.params / args.subgroup))
-    for _ in range(min(args.warmup, 1)):
-        cpu_oracle_rate(sg, 1, args.lowp, threads)
+    for _ in range(args.warmup):  # untimed full steps
+        cpu_oracle_rate(sg, nsub, args.lowp, threads)
     vals, secs = [], 0.0
     for _ in range(args.steps):
         r = cpu_oracle_rate(sg, nsub, args.lowp, threads)
@@ -205,6 +205,383 @@ def run_reference(args, rank: int, world: int) -> None:
 # ---------------------------------------------------------------- B200 arm
 
 
+class B200Bench:
+    """One rank of the B200 arm: a 7B shard (or its ZeRO-3 slice), pinned on
+    the host and attached to the GPU, driven through execute_plan."""
+
+    def __init__(self, args, rank: int, world: int, local: int) -> None:
+        import torch
+        import torch.distributed as dist
+
+        import paper_2410_21316_b200 as D
+        from paper_2410_21316_b200 import policy, profile_b200
+
+        self.args, self.rank, self.world = args, rank, world
+        self.torch, self.dist, self.D, self.policy, self.profile_b200 = torch, dist, D, policy, profile_b200
+        torch.cuda.set_device(local)
+        self.device = torch.device("cuda", local)
+        if world > 1:
+            dist.init_process_group("nccl", device_id=self.device)
+            D._native.lib().dos_set_host_threads(max(1, len(os.sched_getaffinity(0)) // world))
+        if args.host_threads > 0:
+            D._native.lib().dos_set_host_threads(args.host_threads)
+        self.P, self.SG = int(args.params), int(args.subgroup)
+        self.hyper = D.AdamHyper()
+        self.out: dict = {}
+
+    # -- collective helpers (no-ops at N=1)
+    def barrier(self) -> None:
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max_over_ranks(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device=self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def broadcast(self, obj):
+        if self.world == 1:
+            return obj
+        box = [obj]
+        self.dist.broadcast_object_list(box, src=0)
+        return box[0]
+
+    def timed(self, fn, steps: int) -> float:
+        """ms per step of ``fn``, CUDA events, synchronised, max over ranks."""
+        torch = self.torch
+        self.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return self.max_over_ranks(e0.elapsed_time(e1) / steps)
+
+    # -- phases of the run
+    def cpu_baseline(self) -> None:
+        """The oracle port on the host cores, before the pinned shard exists (rank 0, N=1)."""
+        if self.rank != 0 or self.world != 1:
+            self.out["cpu_baseline"] = None
+            return
+        a = self.args
+        threads = len(os.sched_getaffinity(0))
+        r = cpu_oracle_rate(self.SG, a.cpu_sample, a.lowp, threads)
+        self.out["cpu_baseline"] = {
+            "value": r["value"], "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{a.cpu_sample} x {a.subgroup:.0e}-param subgroups ({r['seconds']:.1f} s), "
+                      f"oracle/adam_oracle.c (reference loop restated) with {threads} threads"}
+
+    def setup(self) -> None:
+        D = self.D
+        mine = D.shard(self.P, self.world, self.SG)[self.rank]
+        self.P_rank = sum(g.size for g in mine)
+        t0 = time.perf_counter()
+        self.opt = D.ShardedOptimizer.allocate(self.P_rank, self.SG, lowp=self.args.lowp)
+        t1 = time.perf_counter()
+        fill_shard(self.opt, seed=1234 + self.rank, device=self.device)
+        self.opt.to_device(self.device)
+        self.out["setup_s"] = {"alloc_pin": t1 - t0, "fill": time.perf_counter() - t1}
+        self.sizes = [g.size for g in self.opt.subgroups]
+        self.nsg = len(self.sizes)
+        cap = None if self.args.capacity_gb is None else int(self.args.capacity_gb * 1e9)
+        self.cap = cap
+        self.profile = self.profile_b200.measure_profile(fast_capacity_bytes=cap, quick=True)
+
+    def choose_plan(self) -> None:
+        """Reference planner's choice for one calibration step, re-fit, then
+        explore-then-exploit the stride by measured span (untimed)."""
+        D, a = self.D, self.args
+        choice = D.optimal_stride(self.profile, self.nsg, self.SG)
+        self.choice = choice
+        self.stride_spans = self.tuned = None
+        if a.stride == "auto":
+            stride = choice.k
+        elif a.stride == "all_cpu":
+            stride = D.ALL_CPU
+        else:
+            stride = int(a.stride)
+        self.plan = D.build_plan(self.nsg, stride, static_ratio=a.static_ratio)
+        if a.stride == "auto":
+            r = D.execute_plan(self.opt, self.plan, self.profile, self.hyper)
+            self.profile = self.broadcast(self.policy.refit_profile(self.profile, r.measured, self.sizes))
+            tuner = self.tune(a.static_ratio, explore=4)
+            self.stride_spans = tuner.predicted
+            self.plan = tuner.plan()
+            self.tuned = {str(k): v / 1e6 for k, v in sorted(tuner.measured.items())}
+        self.stride = self.plan.stride
+
+    def tune(self, ratio: float, explore: int):
+        D = self.D
+        tuner = self.policy.StrideTuner(self.profile, self.sizes, range(1, 7), ratio, explore=explore)
+        tuner.queue = list(self.broadcast(tuner.queue))  # same exploration order on every rank
+        while tuner.exploring:
+            k = tuner.next_stride()
+            r = D.execute_plan(self.opt, D.build_plan(self.nsg, k, static_ratio=ratio), self.profile, self.hyper)
+            tuner.record(k, self.max_over_ranks(r.measured.span_ns))
+        return tuner
+
+    def run_timed(self) -> None:
+        """W warm-up steps, then exactly K timed steps (device-resident grads)."""
+        torch, D, a = self.torch, self.D, self.args
+        for _ in range(a.warmup):
+            D.execute_plan(self.opt, self.plan, self.profile, self.hyper)
+        clocks = ClockSampler(self.device.index)
+        self.barrier()
+        torch.cuda.synchronize()
+        clocks.start()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        self.results = []
+        launches0 = D._native.lib().dos_launch_count()
+        torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include timed/ captures exactly this region
+        e0.record()
+        for _ in range(a.steps):
+            self.results.append(D.execute_plan(self.opt, self.plan, self.profile, self.hyper))
+        e1.record()
+        torch.cuda.nvtx.range_pop()
+        torch.cuda.synchronize()
+        self.barrier()
+        self.out["clocks"] = clocks.stop()
+        self.out["gpu_launches"] = D._native.lib().dos_launch_count() - launches0
+        self.ms = self.max_over_ranks(e0.elapsed_time(e1) / a.steps)
+
+    def rooflines(self) -> None:
+        """K1 from the measured GPU_UPDATE events; the phase against HBM,
+        link and host-DRAM bounds."""
+        D, opt, plan = self.D, self.opt, self.plan
+        k1_ns = k1_params = k1_n = 0
+        lane_busy: dict = {}
+        for r in self.results:
+            for ev in r.measured.events:
+                if ev.action.kind is D.ActionKind.GPU_UPDATE:
+                    k1_ns += ev.duration_ns
+                    k1_params += opt.subgroups[ev.action.subgroup].size
+                    k1_n += 1
+            for lane, b in r.measured.lane_busy_ns.items():
+                lane_busy[lane.value] = lane_busy.get(lane.value, 0) + b
+        pred = self.results[0].timeline
+        self.h2d_b = sum(ev.bytes for ev in pred.events if ev.action.lane.value == "h2d")
+        self.d2h_b = sum(ev.bytes for ev in pred.events if ev.action.lane.value == "d2h")
+        peaks_f = ROOT / "MEASURED_PEAKS.json"
+        hbm_peak = float(json.loads(peaks_f.read_text()).get("hbm_gbs", 6650.0)) if peaks_f.exists() else 6650.0
+        k1_gbs = BYTES_PER_PARAM_K1 * k1_params / (k1_ns * 1e-9) / 1e9 if k1_ns else None
+        tf = ROOT / "profiles" / "k1_ncu_summary.json"
+        traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch") if tf.exists() else None
+        self.out["k1_updates"] = k1_n
+        self.out["roofline"] = {
+            "bound": "hbm", "achieved": k1_gbs, "peak": hbm_peak, "unit": "GB/s",
+            "frac": (k1_gbs / hbm_peak) if k1_gbs else None, "traffic": traffic,
+            "kernel": "K1 k_adam_tma (fused Adam + bf16 working copy, TMA ring)",
+            "bytes_per_param": BYTES_PER_PARAM_K1,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks_f.exists() else "fallback 6.65 TB/s"}
+        # phase: HBM time of the fast-tier params, busier link direction at the
+        # measured per-direction rate, host DRAM (24 B per streamed param of DMA,
+        # 28 B per host-updated param of H1 + 2 B read by its H2D_PARAMS16) at the
+        # rate measured for H1 + duplex DMA sharing the host memory
+        prof = self.profile
+        fast = sum(self.sizes[i] for i, d in enumerate(plan.devices) if d is D.Device.FAST)
+        static = sum(self.sizes[i] for i in plan.static_set)
+        cpu = self.P_rank - fast
+        host_bytes = 24 * (fast - static) + 30 * cpu
+        link_Bps = prof.channel_params_per_s * 4.0
+        dram_Bps = self.profile_b200.LAST_RAW.get("h1_with_dma", {}).get("host_dram_GBs_combined", 0.0) * 1e9
+        bounds = {"hbm": BYTES_PER_PARAM_K1 * fast / (hbm_peak * 1e9),
+                  "link": max(self.h2d_b, self.d2h_b) / link_Bps,
+                  "host_dram": host_bytes / dram_Bps if dram_Bps else 0.0}
+        bound = max(bounds, key=bounds.get)
+        self.out["phase_roofline"] = {
+            "bound": bound, "ideal_ms": bounds[bound] * 1e3, "achieved_ms": self.ms,
+            "frac": bounds[bound] * 1e3 / self.ms, "bounds_ms": {k: v * 1e3 for k, v in bounds.items()},
+            "link_GBs_per_dir_measured": link_Bps / 1e9, "host_dram_bytes_per_step": host_bytes,
+            "host_dram_GBs_measured": dram_Bps / 1e9,
+            "host_update_ms_at_measured_rate": cpu / prof.cpu_update_params_per_s * 1e3}
+        spans = [r.measured.span_ns for r in self.results]
+        self.out["iteration"] = {
+            "update_span_ms_median": float(np.median(spans)) / 1e6,
+            "update_makespan_ms_median": float(np.median([r.measured.makespan_ns for r in self.results])) / 1e6,
+            "predicted_makespan_ms": pred.makespan_ns / 1e6, "predicted_span_ms": pred.span_ns / 1e6,
+            "lane_busy_ms_per_step": {k: v / 1e6 / len(self.results) for k, v in lane_busy.items()},
+            "h2d_bytes_per_step": self.h2d_b, "d2h_bytes_per_step": self.d2h_b}
+
+    def grad_flush(self) -> None:
+        """§8(f) row 1: the host lane needs the host subgroups' grads — flushed
+        D2H before the phase, and alternatively inside it (flush_grads)."""
+        torch, D, opt = self.torch, self.D, self.opt
+        cpu_sgs = [g for i, g in enumerate(opt.subgroups) if self.plan.devices[i] is D.Device.CPU]
+        dev_g16 = opt.residency.grads.view(torch.int16)
+        host_g16 = torch.from_numpy(opt._g.view(np.int16))
+
+        def flush():
+            for g in cpu_sgs:
+                host_g16[g.start:g.stop].copy_(dev_g16[g.start:g.stop], non_blocking=True)
+
+        flush_ms = self.timed(flush, 1)
+        D.execute_plan(opt, self.plan, self.profile, self.hyper, flush_grads=True)
+        in_phase = self.timed(lambda: D.execute_plan(opt, self.plan, self.profile, self.hyper, flush_grads=True),
+                              self.args.steps)
+        self.out["iteration"].update({
+            "grad_flush_ms": flush_ms, "grad_flush_bytes": 2 * sum(g.size for g in cpu_sgs),
+            "phase_with_in_phase_grad_flush_ms": in_phase,
+            # the update part of an iteration: grad flush + phase (+ RS at N>1; the
+            # all-gather is overlapped or fused), flush before or inside the phase
+            "iteration_update_ms": min(flush_ms + self.ms, in_phase)})
+
+    def e2e(self) -> None:
+        """Through the public API with host buffers: grads read from pinned
+        host memory, working copy mirrored back (execute_plan host_io=True)."""
+        if self.args.no_e2e:
+            self.out["e2e"] = None
+            return
+        D, opt, plan = self.D, self.opt, self.plan
+        fast = sum(s for i, s in enumerate(self.sizes) if plan.devices[i] is D.Device.FAST)
+        D.execute_plan(opt, plan, self.profile, self.hyper, host_io=True)  # warm the mode
+        ms = self.timed(lambda: D.execute_plan(opt, plan, self.profile, self.hyper, host_io=True), self.args.steps)
+        self.out["e2e"] = {
+            "value": self.P / (ms * 1e-3), "unit": UNIT,
+            "h2d_bytes_per_step": (2 * fast + self.h2d_b) * self.world,
+            "d2h_bytes_per_step": (2 * fast + self.d2h_b) * self.world, "ms_per_step": ms,
+            "api": "execute_plan(..., host_io=True): grads from pinned host, working copy back to host",
+            "host_resident_params": (self.P_rank - fast) * self.world}
+
+    def collectives(self) -> None:
+        """N > 1: bucketed NCCL reduce-scatter of the grads, the all-gather of
+        the working copy (alone, chained onto engine events, and fused into K1)."""
+        self.out["collectives"] = None
+        if self.world == 1:
+            return
+        torch, D = self.torch, self.D
+        from paper_2410_21316_b200.distributed import (BucketedCollectives, PeerTargets, ShardLayout,
+                                                       gather_params_overlapped)
+
+        lay = ShardLayout.build(self.P, self.world, self.SG)
+        coll = BucketedCollectives(lay)
+        tdt = torch.bfloat16 if self.args.lowp == "bf16" else torch.float16
+        full = torch.zeros(lay.padded_total, dtype=tdt, device=self.device)
+        mine = torch.zeros(lay.per_rank, dtype=tdt, device=self.device)
+        coll.reduce_scatter_all(full, mine)
+        coll.all_gather_all(full, mine)
+        rs_ms = self.timed(lambda: coll.reduce_scatter_all(full, mine), 1)
+        ag_ms = self.timed(lambda: coll.all_gather_all(full, mine), 1)
+
+        def overlapped():
+            hook = gather_params_overlapped(coll, self.plan, self.opt.residency.model16, full)
+            D.execute_plan(self.opt, self.plan, self.profile, self.hyper, on_submitted=hook)
+            for w in hook.works:
+                if w is not None:
+                    w.wait()
+
+        phase_ag = self.timed(overlapped, 1)
+        peers, why = None, ""
+        try:
+            peers = PeerTargets(full, lay)
+        except Exception as exc:  # e.g. no P2P between these GPUs
+            why = str(exc)[:160]
+        # every rank must agree before anyone waits in the fused phase's barrier
+        if -self.max_over_ranks(-1.0 if peers is not None else 0.0) >= 1.0:
+            def fused():
+                D.execute_plan(self.opt, self.plan, self.profile, self.hyper, peers=peers.targets)
+                peers.barrier()
+
+            fused_ms = self.timed(fused, 1)
+        else:
+            fused_ms = f"unavailable: {why or 'a peer could not map the IPC buffers'}"
+        best = min(phase_ag, fused_ms) if isinstance(fused_ms, float) else phase_ag
+        self.out["collectives"] = {
+            "reduce_scatter_ms": rs_ms, "all_gather_ms": ag_ms, "buckets": lay.num_buckets,
+            "bytes_per_rank_each": 2 * lay.padded_total,
+            "phase_with_overlapped_all_gather_ms": phase_ag, "phase_with_fused_all_gather_ms": fused_ms,
+            "iteration_update_ms": rs_ms + best}
+        self.out["iteration"]["iteration_update_ms"] += rs_ms
+
+    def static_variants(self) -> None:
+        """the same phase with a fraction of the subgroups'
+        fp32 state resident in HBM (0% = the paper's pure offload)."""
+        D = self.D
+        variants = []
+        for tok in [t for t in self.args.static_variants.split(",") if t.strip()]:
+            ratio = float(tok)
+            tuner = self.tune(ratio, explore=3)  # untimed; the first step also moves the residents
+            vplan = tuner.plan()
+            D.execute_plan(self.opt, vplan, self.profile, self.hyper)
+            ms = self.timed(lambda: D.execute_plan(self.opt, vplan, self.profile, self.hyper), self.args.steps)
+            variants.append({"static_ratio": ratio, "stride": vplan.stride, "ms_per_step": ms,
+                             "value": self.P / (ms * 1e-3),
+                             "hbm_resident_state_bytes": 12 * sum(self.sizes[i] for i in vplan.static_set) * self.world})
+        self.out["static_variants"] = variants
+
+    def reference_schedule(self) -> None:
+        """The reference's offload-to-CPU schedule (ALL_CPU blocking plan,
+        scheduler.py:301-319) executed by this runtime on the same box."""
+        if self.args.no_ref_schedule:
+            self.out["reference_offload_schedule"] = None
+            return
+        D = self.D
+        rplan = D.build_plan(self.nsg, D.ALL_CPU)
+        D.execute_plan(self.opt, rplan, self.profile, self.hyper)
+        ms = self.timed(lambda: D.execute_plan(self.opt, rplan, self.profile, self.hyper), 2)
+        self.out["reference_offload_schedule"] = {
+            "ms_per_step": ms, "value": self.P / (ms * 1e-3), "speedup_of_headline": ms / self.ms,
+            "plan": "build_plan(N, ALL_CPU): CPU_UPDATE -> CPU_DOWNSCALE -> H2D_PARAMS16 chained"}
+
+    def traces(self) -> None:
+        if self.rank != 0 or not self.args.trace_dir:
+            return
+        from paper_2410_21316_b200.timing import write_trace_csv
+
+        os.makedirs(self.args.trace_dir, exist_ok=True)
+        tag = f"{self.P / 1e9:g}B_stride{self.stride}"
+        for kind, tl in (("measured", self.results[-1].measured), ("predicted", self.results[-1].timeline)):
+            with open(os.path.join(self.args.trace_dir, f"{kind}_{tag}.csv"), "w") as fh:
+                write_trace_csv(tl, fh)
+
+    def line(self) -> dict:
+        D, a, prof = self.D, self.args, self.profile
+        windows = 2 if self.cap is None else min(2, self.cap // (12 * self.SG))
+        config = {
+            "workload": f"{self.P / 1e9:g}B-param fp32 Adam shard, {a.lowp} grads + working copy, "
+                        f"host offload of {100 * (1 - a.static_ratio):g}% of the optimizer state "
+                        f"({100 * a.static_ratio:g}% HBM-resident, TwinFlow-style) (BASELINE configs[1])",
+            "params": self.P, "subgroup": self.SG, "subgroups_per_rank": self.nsg, "lowp": a.lowp,
+            "stride": "all_cpu" if self.stride is D.ALL_CPU else self.stride,
+            "planner_k": "all_cpu" if self.choice.k is D.ALL_CPU else self.choice.k, "k_real": self.choice.k_real,
+            "predicted_span_ms_by_stride": None if self.stride_spans is None else
+            {str(k): v / 1e6 for k, v in self.stride_spans.items()},
+            "measured_span_ms_by_stride": self.tuned, "static_ratio": a.static_ratio,
+            "fast_capacity_bytes": self.cap, "hbm_windows": windows,
+            "parallelism": f"zero3-shard{self.world}", "l2": "inputs > L2 (28 B/param over 1e8-param subgroups)"}
+        line = {"metric": METRIC, "value": self.P / (self.ms * 1e-3), "unit": UNIT, "n_gpus": self.world,
+                "steps": a.steps, "warmup": a.warmup, "ms_per_step": self.ms, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (seeded, generated on device)", "config": config}
+        line.update(self.out)
+        line["profile"] = {"channel_params_per_s": prof.channel_params_per_s,
+                           "fast_update_params_per_s": prof.fast_update_params_per_s,
+                           "cpu_update_params_per_s": prof.cpu_update_params_per_s,
+                           "host_contention": prof.host_contention,
+                           "host_threads": D._native.lib().dos_host_threads()}
+        return line
+
+    def run(self) -> None:
+        self.cpu_baseline()
+        self.setup()
+        self.choose_plan()
+        self.run_timed()
+        self.rooflines()
+        self.grad_flush()
+        self.e2e()
+        self.collectives()
+        self.static_variants()
+        self.reference_schedule()
+        self.traces()
+        if self.rank == 0:
+            print(json.dumps(self.line()), flush=True)
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
 def main() -> None:
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -213,423 +590,7 @@ def main() -> None:
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-
-    import torch
-    import torch.distributed as dist
-
-    import paper_2410_21316_b200 as D
-    from paper_2410_21316_b200 import policy, profile_b200
-    from paper_2410_21316_b200.plan import ActionKind
-
-    torch.cuda.set_device(local)
-    device = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=device)
-        D._native.lib().dos_set_host_threads(max(1, len(os.sched_getaffinity(0)) // world))
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    if args.host_threads > 0:
-        D._native.lib().dos_set_host_threads(args.host_threads)
-    P = int(args.params)
-    SG = int(args.subgroup)
-    mine = D.shard(P, world, SG)[rank]
-    P_rank = sum(g.size for g in mine)
-    # CPU baseline first (rank 0, N=1): the oracle port on the host cores,
-    # measured before the 112 GB pinned shard exists, like the reference arm.
-    cpu_baseline = None
-    if rank == 0 and world == 1:
-        threads = len(os.sched_getaffinity(0))
-        r = cpu_oracle_rate(int(args.subgroup), args.cpu_sample, args.lowp, threads)
-        cpu_baseline = {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "port",
-                        "sample": f"{args.cpu_sample} x {args.subgroup:.0e}-param subgroups ({r['seconds']:.1f} s), "
-                                  f"oracle/adam_oracle.c (reference loop restated) with {threads} threads"}
-    t_setup = time.perf_counter()
-    opt = D.ShardedOptimizer.allocate(P_rank, SG, lowp=args.lowp)
-    t_alloc = time.perf_counter() - t_setup
-    fill_shard(opt, seed=1234 + rank, device=device)
-    opt.to_device(device)
-    t_fill = time.perf_counter() - t_setup - t_alloc
-
-    cap = None if args.capacity_gb is None else int(args.capacity_gb * 1e9)
-    profile = profile_b200.measure_profile(fast_capacity_bytes=cap, quick=True)
-    nsg = len(opt.subgroups)
-    sizes = [g.size for g in opt.subgroups]
-    hyper = D.AdamHyper()
-    # The reference planner's choice (Eq. 1 + the k-as-stride rule) runs the
-    # first warm-up step; its measured timeline re-fits the constants and the
-    # B200 policy picks the stride for the rest (per-iteration re-fit).
-    choice = D.optimal_stride(profile, nsg, SG)
-    planner_stride = choice.k
-    stride_spans = None
-    if args.stride == "auto":
-        stride = planner_stride
-    elif args.stride == "all_cpu":
-        stride = D.ALL_CPU
-    else:
-        stride = int(args.stride)
-    plan = D.build_plan(nsg, stride, static_ratio=args.static_ratio)
-    tuned = None
-    if args.stride == "auto":
-        # calibration (untimed, before the warm-up): one step on the reference
-        # planner's plan, re-fit the constants from its measured timeline, then
-        # explore the model's best candidates by measurement (StrideTuner).
-        r = D.execute_plan(opt, plan, profile, hyper)
-        profile = policy.refit_profile(profile, r.measured, sizes)
-        if world > 1:  # every rank must explore the same candidates in the same order
-            box = [profile]
-            dist.broadcast_object_list(box, src=0)
-            profile = box[0]
-        tuner = policy.StrideTuner(profile, sizes, range(1, 7), args.static_ratio, explore=4)
-        if world > 1:
-            box = [tuner.queue]
-            dist.broadcast_object_list(box, src=0)
-            tuner.queue = list(box[0])
-        stride_spans = tuner.predicted
-        while tuner.exploring:
-            k = tuner.next_stride()
-            r = D.execute_plan(opt, D.build_plan(nsg, k, static_ratio=args.static_ratio), profile, hyper)
-            tuner.record(k, max_over_ranks(r.measured.span_ns))
-        stride = tuner.next_stride()
-        plan = tuner.plan()
-        tuned = {str(k): v / 1e6 for k, v in sorted(tuner.measured.items())}
-    for w in range(args.warmup):
-        D.execute_plan(opt, plan, profile, hyper)
-    torch.cuda.synchronize()
-
-    # ---------------- timed region: device-resident grads (value)
-    clocks = ClockSampler(device.index)
-    barrier()
-    torch.cuda.synchronize()
-    clocks.start()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    results = []
-    launches0 = D._native.lib().dos_launch_count()
-    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include timed/ captures exactly this region
-    e0.record()
-    for _ in range(args.steps):
-        results.append(D.execute_plan(opt, plan, profile, hyper))
-    e1.record()
-    torch.cuda.nvtx.range_pop()
-    torch.cuda.synchronize()
-    barrier()
-    clk = clocks.stop()
-    ms = e0.elapsed_time(e1) / args.steps
-    ms_max = max_over_ranks(ms)
-    value = P / (ms_max * 1e-3)
-
-    # per-step measured phase, K1 roofline from the measured GPU_UPDATE events
-    spans = [r.measured.span_ns for r in results]
-    makespans = [r.measured.makespan_ns for r in results]
-    gpu_launches = D._native.lib().dos_launch_count() - launches0  # libdos kernels in the timed region
-    k1_ns, k1_params, k1_launches = 0, 0, 0
-    h2d_b = d2h_b = 0
-    lane_busy = {}
-    for r in results:
-        for ev in r.measured.events:
-            a = ev.action
-            if a.kind is ActionKind.GPU_UPDATE:
-                k1_ns += ev.duration_ns
-                k1_params += opt.subgroups[a.subgroup].size
-                k1_launches += 1
-        for lane, b in r.measured.lane_busy_ns.items():
-            lane_busy[lane.value] = lane_busy.get(lane.value, 0) + b
-    for ev in results[0].timeline.events:
-        if ev.action.lane.value == "h2d":
-            h2d_b += ev.bytes
-        elif ev.action.lane.value == "d2h":
-            d2h_b += ev.bytes
-    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    k1_gbs = BYTES_PER_PARAM_K1 * k1_params / (k1_ns * 1e-9) / 1e9 if k1_ns else None
-    traffic = None
-    tf = ROOT / "profiles" / "k1_ncu_summary.json"
-    if tf.exists():
-        traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
-
-    # phase roofline: the slower of HBM time for the fast-tier params and the
-    # busier link direction at the measured per-direction rate (north_star)
-    link_Bps = profile.channel_params_per_s * 4.0
-    fast_params = sum(opt.subgroups[i].size for i, d in enumerate(plan.devices) if d is D.Device.FAST)
-    t_hbm = BYTES_PER_PARAM_K1 * fast_params / (hbm_peak * 1e9)
-    t_link = max(h2d_b, d2h_b) / link_Bps
-    t_host = (P_rank - fast_params) / profile.cpu_update_params_per_s
-    # host DRAM: every streamed param costs 24 B of DMA (12 read + 12 written),
-    # every host-updated param 28 B of H1 traffic + 2 B read by its H2D_PARAMS16;
-    # rate = measured H1 + duplex DMA sharing the host memory (profile_b200)
-    static_params = sum(opt.subgroups[i].size for i in plan.static_set)
-    dyn_fast = fast_params - static_params
-    cpu_params = P_rank - fast_params
-    host_bytes = 24 * dyn_fast + 30 * cpu_params
-    dram_Bps = profile_b200.LAST_RAW.get("h1_with_dma", {}).get("host_dram_GBs_combined", 0.0) * 1e9
-    t_dram = host_bytes / dram_Bps if dram_Bps else 0.0
-    bounds = {"hbm": t_hbm, "link": t_link, "host_dram": t_dram}
-    phase_bound = max(bounds, key=bounds.get)
-    phase_ideal = bounds[phase_bound]
-
-    # ---------------- iteration time = grad flush + update span (+ RS/AG at N>1):
-    # the host lane reads the bf16 grads of host-scheduled subgroups, so they
-    # are flushed D2H (pinned) before the phase (§8(f) row 1; in training this
-    # overlaps the backward pass — reported separately, not hidden)
-    cpu_sgs = [g for i, g in enumerate(opt.subgroups) if plan.devices[i] is D.Device.CPU]
-    dev_g16 = opt.residency.grads.view(torch.int16)
-    host_g16 = torch.from_numpy(opt._g.view(np.int16))
-    fl0, fl1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    fl0.record()
-    for g in cpu_sgs:
-        host_g16[g.start:g.stop].copy_(dev_g16[g.start:g.stop], non_blocking=True)
-    fl1.record()
-    torch.cuda.synchronize()
-    flush_ms = max_over_ranks(fl0.elapsed_time(fl1))
-    flush_bytes = 2 * sum(g.size for g in cpu_sgs)
-    # ... and the same flush moved inside the phase (per-subgroup D2H on its
-    # own stream, each CPU_UPDATE waiting only for its own grads)
-    D.execute_plan(opt, plan, profile, hyper, flush_grads=True)
-    barrier()
-    torch.cuda.synchronize()
-    fl0.record()
-    for _ in range(args.steps):
-        D.execute_plan(opt, plan, profile, hyper, flush_grads=True)
-    fl1.record()
-    torch.cuda.synchronize()
-    in_phase_flush_ms = max_over_ranks(fl0.elapsed_time(fl1) / args.steps)
-
-    # ---------------- e2e through the public API with host buffers
-    e2e = None
-    if not args.no_e2e:
-        # host_io mode: grads are read from the pinned host image; fast
-        # subgroups ship theirs H2D inside their prefetch, and the working
-        # copy is mirrored back inside the flushes (include/dos.h host_io).
-        fast_params = sum(s for i, s in enumerate(sizes) if plan.devices[i] is D.Device.FAST)
-        cpu_params = P_rank - fast_params
-        h2d_e2e = 2 * fast_params + sum(ev.bytes for ev in results[0].timeline.events if ev.action.lane.value == "h2d")
-        d2h_e2e = 2 * fast_params + sum(ev.bytes for ev in results[0].timeline.events if ev.action.lane.value == "d2h")
-        D.execute_plan(opt, plan, profile, hyper, host_io=True)  # warm the mode
-        barrier()
-        torch.cuda.synchronize()
-        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        f0.record()
-        for _ in range(args.steps):
-            D.execute_plan(opt, plan, profile, hyper, host_io=True)
-        f1.record()
-        torch.cuda.synchronize()
-        barrier()
-        e2e_ms = max_over_ranks(f0.elapsed_time(f1) / args.steps)
-        e2e = {"value": P / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d_e2e * world,
-               "d2h_bytes_per_step": d2h_e2e * world, "ms_per_step": e2e_ms,
-               "api": "execute_plan(..., host_io=True): grads from pinned host, working copy back to host",
-               "host_resident_params": cpu_params * world}
-
-    # ---------------- iteration collectives (N > 1): bucketed NCCL reduce-scatter
-    # of bf16 grads before the phase and all-gather of the bf16 working copy after
-    collectives = None
-    if world > 1:
-        from paper_2410_21316_b200.distributed import BucketedCollectives, ShardLayout
-
-        lay = ShardLayout.build(P, world, SG)
-        coll = BucketedCollectives(lay)
-        tdt = torch.bfloat16 if args.lowp == "bf16" else torch.float16
-        full = torch.zeros(lay.padded_total, dtype=tdt, device=device)
-        mine_buf = torch.zeros(lay.per_rank, dtype=tdt, device=device)
-        coll.reduce_scatter_all(full, mine_buf)
-        coll.all_gather_all(full, mine_buf)
-        torch.cuda.synchronize()
-        c0, c1, c2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-        barrier()
-        c0.record()
-        coll.reduce_scatter_all(full, mine_buf)
-        c1.record()
-        coll.all_gather_all(full, mine_buf)
-        c2.record()
-        torch.cuda.synchronize()
-        rs_ms, ag_ms = max_over_ranks(c0.elapsed_time(c1)), max_over_ranks(c1.elapsed_time(c2))
-        # the phase with every bucket's all-gather chained onto the engine event
-        # that finalises its subgroup (overlapped with the rest of the phase)
-        from paper_2410_21316_b200.distributed import gather_params_overlapped
-
-        hook = gather_params_overlapped(coll, plan, opt.residency.model16, full)
-        barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        D.execute_plan(opt, plan, profile, hyper, on_submitted=hook)
-        for w in hook.works:
-            if w is not None:
-                w.wait()
-        torch.cuda.synchronize()
-        phase_ag_ms = max_over_ranks((time.perf_counter() - t0) * 1e3)
-        # fused: K1 stores the working copy into every peer's full buffer (IPC / NVLink)
-        fused_ms, peers, why = None, None, ""
-        try:
-            from paper_2410_21316_b200.distributed import PeerTargets
-
-            peers = PeerTargets(full, lay)
-        except Exception as exc:  # e.g. no P2P between these GPUs
-            why = str(exc)[:160]
-        # every rank must agree before anyone waits in the fused phase's barrier
-        all_ok = -max_over_ranks(-1.0 if peers is not None else 0.0) >= 1.0
-        if all_ok:
-            barrier()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            D.execute_plan(opt, plan, profile, hyper, peers=peers.targets)
-            peers.barrier()
-            fused_ms = max_over_ranks((time.perf_counter() - t0) * 1e3)
-        else:
-            fused_ms = f"unavailable: {why or 'a peer could not map the IPC buffers'}"
-        collectives = {"reduce_scatter_ms": rs_ms, "all_gather_ms": ag_ms, "buckets": lay.num_buckets,
-                       "bytes_per_rank_each": 2 * lay.padded_total,
-                       "phase_with_overlapped_all_gather_ms": phase_ag_ms,
-                       "phase_with_fused_all_gather_ms": fused_ms,
-                       "iteration_update_ms": rs_ms + min(phase_ag_ms, fused_ms if isinstance(fused_ms, float)
-                                                          else phase_ag_ms)}
-        del full, mine_buf
-
-    # ---------------- static-resident variants: the same
-    # 7B phase with a fraction of subgroups' fp32 state resident in HBM
-    variants = []
-    for tok in [t for t in args.static_variants.split(",") if t.strip()]:
-        ratio = float(tok)
-        vt = policy.StrideTuner(profile, sizes, range(1, 7), ratio, explore=3)
-        if world > 1:
-            box = [vt.queue]
-            dist.broadcast_object_list(box, src=0)
-            vt.queue = list(box[0])
-        while vt.exploring:  # untimed; the first step also moves the residents into HBM
-            k = vt.next_stride()
-            r = D.execute_plan(opt, D.build_plan(nsg, k, static_ratio=ratio), profile, hyper)
-            vt.record(k, max_over_ranks(r.measured.span_ns))
-        vstride, vplan = vt.next_stride(), vt.plan()
-        D.execute_plan(opt, vplan, profile, hyper)
-        barrier()
-        torch.cuda.synchronize()
-        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        g0.record()
-        for _ in range(args.steps):
-            D.execute_plan(opt, vplan, profile, hyper)
-        g1.record()
-        torch.cuda.synchronize()
-        vms = max_over_ranks(g0.elapsed_time(g1) / args.steps)
-        variants.append({"static_ratio": ratio, "stride": vstride, "ms_per_step": vms, "value": P / (vms * 1e-3),
-                         "hbm_resident_state_bytes": 12 * sum(sizes[i] for i in vplan.static_set) * world})
-    # the reference's own offload-to-CPU schedule (ALL_CPU blocking plan,
-    # scheduler.py:301-319: update, downscale, H2D of the half-precision
-    # params, serialised per subgroup) executed by this runtime on the same
-    # box — the denominator of the north star's ">= 2x lower update time"
-    ref_sched = None
-    if not args.no_ref_schedule:
-        rplan = D.build_plan(nsg, D.ALL_CPU)
-        D.execute_plan(opt, rplan, profile, hyper)
-        barrier()
-        torch.cuda.synchronize()
-        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        h0.record()
-        for _ in range(2):
-            D.execute_plan(opt, rplan, profile, hyper)
-        h1.record()
-        torch.cuda.synchronize()
-        rms = max_over_ranks(h0.elapsed_time(h1) / 2)
-        ref_sched = {"ms_per_step": rms, "value": P / (rms * 1e-3),
-                     "speedup_of_headline": rms / ms_max,
-                     "plan": "build_plan(N, ALL_CPU): CPU_UPDATE -> CPU_DOWNSCALE -> H2D_PARAMS16 chained"}
-    if variants:
-        opt.residency.set_static(plan.static_set)  # back to the headline placement
-        torch.cuda.empty_cache()
-
-    if rank == 0 and args.trace_dir:
-        from paper_2410_21316_b200.timing import write_trace_csv
-
-        os.makedirs(args.trace_dir, exist_ok=True)
-        tag = f"{P / 1e9:g}B_stride{stride}"
-        with open(os.path.join(args.trace_dir, f"measured_{tag}.csv"), "w") as fh:
-            write_trace_csv(results[-1].measured, fh)
-        with open(os.path.join(args.trace_dir, f"predicted_{tag}.csv"), "w") as fh:
-            write_trace_csv(results[-1].timeline, fh)
-
-    if rank == 0:
-        line = {
-            "metric": METRIC,
-            "value": value,
-            "unit": UNIT,
-            "n_gpus": world,
-            "steps": args.steps,
-            "warmup": args.warmup,
-            "ms_per_step": ms_max,
-            "higher_is_better": True,
-            "scaling": "strong",
-            "vs_baseline": None,
-            "dtype": "f32",
-            "data": "synthetic (seeded, generated on device)",
-            "config": {
-                "workload": f"{P / 1e9:g}B-param fp32 Adam shard, {args.lowp} grads + working copy, "
-                            f"host offload of {100 * (1 - args.static_ratio):g}% of the optimizer state "
-                            f"({100 * args.static_ratio:g}% HBM-resident, TwinFlow-style) (BASELINE configs[1])",
-                "params": P, "subgroup": SG, "subgroups_per_rank": nsg, "lowp": args.lowp,
-                "stride": "all_cpu" if stride is D.ALL_CPU else stride,
-                "planner_k": "all_cpu" if planner_stride is D.ALL_CPU else planner_stride,
-                "k_real": choice.k_real,
-                "predicted_span_ms_by_stride": None if stride_spans is None else
-                {str(k): v / 1e6 for k, v in stride_spans.items()},
-                "measured_span_ms_by_stride": tuned,
-                "static_ratio": args.static_ratio, "fast_capacity_bytes": cap, "hbm_windows": results[0].measured and
-                min(2, 2 if cap is None else cap // (12 * SG)),
-                "parallelism": f"zero3-shard{world}", "l2": "inputs > L2 (28 B/param over 1e8-param subgroups)",
-            },
-            "iteration": {
-                "update_span_ms_median": float(np.median(spans)) / 1e6,
-                "update_makespan_ms_median": float(np.median(makespans)) / 1e6,
-                "predicted_makespan_ms": results[0].timeline.makespan_ns / 1e6,
-                "predicted_span_ms": results[0].timeline.span_ns / 1e6,
-                "lane_busy_ms_per_step": {k: v / 1e6 / len(results) for k, v in lane_busy.items()},
-                "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
-                "grad_flush_ms": flush_ms, "grad_flush_bytes": flush_bytes,
-                "phase_with_in_phase_grad_flush_ms": in_phase_flush_ms,
-                # iteration's update part = grad flush + phase (+ RS at N>1; the
-                # all-gather is overlapped/fused): the better of the flush before
-                # the phase or inside it
-                "iteration_update_ms": min(flush_ms + ms_max, in_phase_flush_ms)
-                + (0.0 if collectives is None else collectives["reduce_scatter_ms"]),
-            },
-            "roofline": {"bound": "hbm", "achieved": k1_gbs, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": (k1_gbs / hbm_peak) if k1_gbs else None, "traffic": traffic,
-                         "kernel": "K1 dos_adam (fused Adam + bf16 copy)",
-                         "bytes_per_param": BYTES_PER_PARAM_K1, "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
-            "phase_roofline": {
-                "bound": phase_bound,
-                "ideal_ms": phase_ideal * 1e3, "achieved_ms": ms_max, "frac": phase_ideal * 1e3 / ms_max,
-                "bounds_ms": {k: v * 1e3 for k, v in bounds.items()},
-                "link_GBs_per_dir_measured": link_Bps / 1e9,
-                "host_dram_bytes_per_step": host_bytes,
-                "host_dram_GBs_measured": dram_Bps / 1e9,
-                "host_update_ms_at_measured_rate": t_host * 1e3,
-            },
-            "cpu_baseline": cpu_baseline,
-            "e2e": e2e,
-            "gpu_launches": gpu_launches,
-            "k1_updates": k1_launches,
-            "clocks": clk,
-            "profile": {"channel_params_per_s": profile.channel_params_per_s,
-                        "fast_update_params_per_s": profile.fast_update_params_per_s,
-                        "cpu_update_params_per_s": profile.cpu_update_params_per_s,
-                        "host_contention": profile.host_contention,
-                        "host_threads": D._native.lib().dos_host_threads()},
-            "setup_s": {"alloc_pin": t_alloc, "fill": t_fill},
-            "static_variants": variants,
-            "reference_offload_schedule": ref_sched,
-            "collectives": collectives,
-        }
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    B200Bench(args, rank, world, local).run()
 
 
 if __name__ == "__main__":
