@@ -64,7 +64,6 @@ def parse():
                     help="skip timing the reference's ALL_CPU offload schedule on this runtime")
     ap.add_argument("--static-variants", default="0.0,0.5,1.0",
                     help="extra measured runs with HBM-resident static subgroups ('' to skip)")
-    ap.add_argument("--profile-out", default=None)
     return ap.parse_args()
 
 
