@@ -315,7 +315,9 @@ class B200Bench:
 
     def tune(self, ratio: float, explore: int):
         D = self.D
-        tuner = self.policy.StrideTuner(self.profile, self.sizes, range(1, 7), ratio, explore=explore)
+        slowdown = float(self.broadcast(self.profile_b200.LAST_RAW.get("link_slowdown_under_h1", 1.0)))
+        tuner = self.policy.StrideTuner(self.profile, self.sizes, range(1, 7), ratio, explore=explore,
+                                        link_slowdown=slowdown)
         tuner.queue = list(self.broadcast(tuner.queue))  # same exploration order on every rank
         while tuner.exploring:
             k = tuner.next_stride()

@@ -64,20 +64,47 @@ def refit_profile(profile: SystemProfile, measured: Timeline, sizes: Sequence[in
     return dataclasses.replace(profile, **upd)
 
 
+def _quiet_plan(n: int, stride, static_ratio: float) -> UpdatePlan:
+    """build_plan without the all-static warning (the policy sweeps ratios
+    up to 1.0 on purpose; the stride is then irrelevant, not a mistake)."""
+    import warnings
+
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)
+        return build_plan(n, stride, static_ratio=static_ratio)
+
+
+_LINK_KINDS = frozenset({ActionKind.PREFETCH_M, ActionKind.PREFETCH_V, ActionKind.PREFETCH_P,
+                         ActionKind.FLUSH_OUT_M, ActionKind.FLUSH_OUT_V, ActionKind.FLUSH_OUT_P,
+                         ActionKind.H2D_PARAMS16})
+
+
 class _B200Durations(SimTarget):
-    """SimTarget durations with the B200's fused actions made free."""
+    """SimTarget durations with the B200's fused actions made free and the
+    host link slowed while the host team competes for host DRAM.
+
+    ``link_slowdown`` is the measured duplex-link ratio alone / under H1
+    (profile_b200.measure_link_under_h1); it applies in proportion to the
+    share of the plan's params the host updates (0 for an all-fast plan)."""
+
+    def __init__(self, profile, plan, sizes, link_slowdown: float = 1.0) -> None:
+        super().__init__(profile, plan, sizes)
+        total = sum(self.sizes) or 1
+        host = sum(s for i, s in enumerate(self.sizes) if plan.devices[i] is Device.CPU)
+        self._link_scale = 1.0 + (max(1.0, link_slowdown) - 1.0) * host / total
 
     def duration_ns(self, action) -> int:
         if action.kind in (ActionKind.FLUSH_OUT_MODEL16, ActionKind.CPU_DOWNSCALE):
             return 0
-        return super().duration_ns(action)
+        d = super().duration_ns(action)
+        return int(d * self._link_scale) if action.kind in _LINK_KINDS else d
 
 
 def simulate_b200_phase(plan: UpdatePlan, profile: SystemProfile, subgroup_size: "int | Sequence[int]",
-                        num_slots: int = 2) -> Timeline:
+                        num_slots: int = 2, link_slowdown: float = 1.0) -> Timeline:
     """Predicted timeline of ``plan`` on the B200 engine (see module doc)."""
     sizes = normalize_sizes(plan, subgroup_size)
-    t = _B200Durations(profile, plan, sizes)
+    t = _B200Durations(profile, plan, sizes, link_slowdown)
     lane_free = dict.fromkeys(Lane, 0)
     finish: list[int] = []
     closes: list[int] = []  # window close times, in opening order
@@ -102,13 +129,13 @@ def simulate_b200_phase(plan: UpdatePlan, profile: SystemProfile, subgroup_size:
 
 
 def choose_stride(profile: SystemProfile, sizes: Sequence[int], candidates: Iterable = range(1, 7),
-                  static_ratio: float = 0.0, num_slots: int = 2):
+                  static_ratio: float = 0.0, num_slots: int = 2, link_slowdown: float = 1.0):
     """Stride with the smallest predicted B200 span; returns (stride, {stride: span_ns})."""
     n = len(sizes)
     spans = {}
     for k in candidates:
-        plan = build_plan(n, k, static_ratio=static_ratio)
-        spans[k] = simulate_b200_phase(plan, profile, list(sizes), num_slots).span_ns
+        plan = _quiet_plan(n, k, static_ratio)
+        spans[k] = simulate_b200_phase(plan, profile, list(sizes), num_slots, link_slowdown).span_ns
     best = min(spans, key=lambda k: (spans[k], 0 if k is ALL_CPU else k))
     return best, spans
 
@@ -126,10 +153,11 @@ class StrideTuner:
     """
 
     def __init__(self, profile: SystemProfile, sizes: Sequence[int], candidates: Iterable = range(1, 7),
-                 static_ratio: float = 0.0, explore: int = 4, num_slots: int = 2) -> None:
+                 static_ratio: float = 0.0, explore: int = 4, num_slots: int = 2,
+                 link_slowdown: float = 1.0) -> None:
         self.sizes = list(sizes)
         self.static_ratio = static_ratio
-        best, spans = choose_stride(profile, self.sizes, candidates, static_ratio, num_slots)
+        best, spans = choose_stride(profile, self.sizes, candidates, static_ratio, num_slots, link_slowdown)
         ranked = sorted(spans, key=lambda k: spans[k])
         self.queue = ranked[:max(1, explore)]
         self.predicted = spans
@@ -150,7 +178,7 @@ class StrideTuner:
         return bool(self.queue)
 
     def plan(self) -> UpdatePlan:
-        return build_plan(len(self.sizes), self.next_stride(), static_ratio=self.static_ratio)
+        return _quiet_plan(len(self.sizes), self.next_stride(), self.static_ratio)
 
 
 def fast_fraction(plan: UpdatePlan, sizes: Sequence[int]) -> float:

@@ -77,6 +77,36 @@ def measure_link(nbytes: int = 1 << 30, reps: int = 3) -> dict:
             "duplex_GBs_per_dir": nbytes / t_dup / 1e9}
 
 
+def measure_link_under_h1(nbytes: int = 1 << 28, n: int = 50_000_000) -> dict:
+    """Duplex link GB/s while H1 runs on every host thread — the copy
+    engines and the host team share the host DRAM, so the link slows."""
+    hb = N.HostBuffer(n * 16)
+    p, m, v = (hb.array(np.float32, n, k * 4 * n) for k in range(3))
+    g, w = hb.array(np.uint16, n, 12 * n), hb.array(np.uint16, n, 14 * n)
+    p[:] = np.float32(0.01)
+    m[:] = 0
+    v[:] = np.float32(1e-5)
+    g[:] = 0x3F80
+    sc = N.scalars(1e-3, 0.9, 0.999, 1e-8, np.float32(0.1), np.float32(0.001))
+    lib = N.lib()
+    stop = threading.Event()
+
+    def hammer():
+        while not stop.is_set():
+            lib.dos_adam_step_host(p.ctypes.data, m.ctypes.data, v.ctypes.data, g.ctypes.data, N.DOS_BF16,
+                                   w.ctypes.data, N.DOS_BF16, n, sc, 0)
+
+    th = threading.Thread(target=hammer, daemon=True)
+    th.start()
+    time.sleep(0.05)
+    try:
+        res = measure_link(nbytes)
+    finally:
+        stop.set()
+        th.join()
+    return res
+
+
 def measure_k1(n: int = 100_000_000, reps: int = 5) -> dict:
     """K1 params/s and achieved HBM GB/s (28 B/param) on one subgroup."""
     torch = _torch()
@@ -195,8 +225,10 @@ def measure_profile(fast_capacity_bytes: int | None = None, save: bool = False, 
         host_contention=contention,
         caveat="measured by profile_b200.measure_profile",
     )
+    link_h1 = measure_link_under_h1(1 << 28)
     LAST_RAW.clear()
-    LAST_RAW.update({"link": link, "k1": k1, "h1_alone": h1_alone, "h1_with_dma": h1_busy})
+    LAST_RAW.update({"link": link, "k1": k1, "h1_alone": h1_alone, "h1_with_dma": h1_busy, "link_under_h1": link_h1,
+                     "link_slowdown_under_h1": max(1.0, link["duplex_GBs_per_dir"] / link_h1["duplex_GBs_per_dir"])})
     if save:
         d = dataclasses.asdict(prof)
         d["raw"] = {"link": link, "k1": k1, "h1_alone": h1_alone, "h1_with_dma": h1_busy,
