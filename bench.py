@@ -321,7 +321,7 @@ class B200Bench:
         tuner.queue = list(self.broadcast(tuner.queue))  # same exploration order on every rank
         while tuner.exploring:
             k = tuner.next_stride()
-            r = D.execute_plan(self.opt, D.build_plan(self.nsg, k, static_ratio=ratio), self.profile, self.hyper)
+            r = D.execute_plan(self.opt, tuner.plan_for(k), self.profile, self.hyper)
             tuner.record(k, self.max_over_ranks(r.measured.span_ns))
         return tuner
 

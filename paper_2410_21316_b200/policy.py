@@ -178,7 +178,10 @@ class StrideTuner:
         return bool(self.queue)
 
     def plan(self) -> UpdatePlan:
-        return _quiet_plan(len(self.sizes), self.next_stride(), self.static_ratio)
+        return self.plan_for(self.next_stride())
+
+    def plan_for(self, stride) -> UpdatePlan:
+        return _quiet_plan(len(self.sizes), stride, self.static_ratio)
 
 
 def fast_fraction(plan: UpdatePlan, sizes: Sequence[int]) -> float:
