@@ -184,6 +184,7 @@ def run_reference(args, rank: int, world: int) -> None:
         vals.append(r["value"])
         secs += r["seconds"]
     value = float(np.median(vals))
+    one = cpu_oracle_rate(sg, 2, args.lowp, 1)  # context: the reference's single-threaded loop
     P = int(args.params)
     sample = (f"{nsub} x {sg:.0e}-param subgroup passes per step = the full {P / 1e9:g}B phase "
               f"(Adam + {args.lowp} working copy, sequential_oracle order), reusing one resident subgroup buffer")
@@ -194,7 +195,8 @@ def run_reference(args, rank: int, world: int) -> None:
         "data": "synthetic (seeded)",
         "config": {"workload": f"{P / 1e9:g}B-param Adam shard, {args.lowp} grads, sg={sg:.0e}, host cores only",
                    "params": P, "subgroup": sg},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+                         "single_thread_value": one["value"]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
