@@ -263,22 +263,38 @@ def flush_gradients(optimizer: ShardedOptimizer, profile: SystemProfile, strateg
     if chunk_bytes < 2:
         raise ValueError("chunk_bytes must hold at least one fp16 element")
     P = optimizer.total_params
-    out = np.empty(P, dtype=np.float32)
     elems = chunk_bytes // 2
     res = optimizer.residency
     g = optimizer.grads16
     if res is not None and strategy is GradFlushStrategy.GPU_UPSCALE_FP32:
+        # chunk-wise on-device upcast double-buffered against
+        # the pinned fp32 D2H: chunk k+1 converts while chunk k crosses the link
         import torch
 
-        buf = torch.empty(min(elems, P), dtype=torch.float32, device=res.device)
+        from .state import pinned_empty
+
+        out = pinned_empty(P, np.float32)
         host = torch.from_numpy(out)
-        stream = torch.cuda.current_stream(res.device).cuda_stream
-        for lo in range(0, P, elems):
+        n_buf = min(elems, P)
+        bufs = [torch.empty(n_buf, dtype=torch.float32, device=res.device) for _ in range(2)]
+        conv = torch.cuda.current_stream(res.device)
+        copy = torch.cuda.Stream(device=res.device)
+        done = [None, None]
+        for k, lo in enumerate(range(0, P, elems)):
             hi = min(lo + elems, P)
-            N.check(N.lib().dos_upscale_cuda(res.grads.data_ptr() + 2 * lo, optimizer.lowp_code, buf.data_ptr(),
-                                             hi - lo, stream))
-            host[lo:hi].copy_(buf[:hi - lo])
+            b = bufs[k % 2]
+            if done[k % 2] is not None:
+                conv.wait_event(done[k % 2])  # the D2H that last read this buffer has finished
+            N.check(N.lib().dos_upscale_cuda(res.grads.data_ptr() + 2 * lo, optimizer.lowp_code, b.data_ptr(),
+                                             hi - lo, conv.cuda_stream))
+            copy.wait_stream(conv)
+            with torch.cuda.stream(copy):
+                host[lo:hi].copy_(b[:hi - lo], non_blocking=True)
+                done[k % 2] = torch.cuda.Event()
+                done[k % 2].record(copy)
+        copy.synchronize()
     else:
+        out = np.empty(P, dtype=np.float32)
         for lo in range(0, P, elems):
             hi = min(lo + elems, P)
             N.check(N.lib().dos_upscale_host(N.ptr(g) + 2 * lo, optimizer.lowp_code, N.ptr(out) + 4 * lo, hi - lo, 0))
