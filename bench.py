@@ -380,6 +380,11 @@ class B200Bench:
             "kernel": "K1 k_adam_tma (fused Adam + bf16 working copy, TMA ring)",
             "bytes_per_param": BYTES_PER_PARAM_K1,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks_f.exists() else "fallback 6.65 TB/s"}
+        # context: the same kernel alone on one 1e8-param subgroup (no concurrent
+        # host-link DMA), CUDA events, median of 10
+        alone = self.profile_b200.measure_k1(self.SG, reps=10)
+        self.out["roofline"]["standalone"] = {"achieved": alone["k1_GBs"], "frac": alone["k1_GBs"] / hbm_peak,
+                                              "ms_per_launch": alone["k1_ms"], "params": alone["n"]}
         # phase: HBM time of the fast-tier params, busier link direction at the
         # measured per-direction rate, host DRAM (24 B per streamed param of DMA,
         # 28 B per host-updated param of H1 + 2 B read by its H2D_PARAMS16) at the
