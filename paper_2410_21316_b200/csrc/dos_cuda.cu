@@ -305,21 +305,35 @@ __device__ __forceinline__ void bulk_wait_read() {
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// Shared memory of one pipeline stage: p, m, v (fp32), the grads (fp32 or
+// 16-bit) and — for fp32 grads only — a separate working-copy slot (16-bit
+// grads are overwritten in place by the working copy).
+template <int GT, int LT, int NT>
+__host__ __device__ constexpr uint32_t tma_stage_bytes() {
+  return 4 * NT * (12 + (GT == DOS_F32 ? 4 : 2) + ((GT == DOS_F32 && LT != DOS_NONE) ? 2 : 0));
+}
+
 template <int GT, int LT, int NT, int S>
 __global__ void __launch_bounds__(NT, 1)
     k_adam_tma(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
-               const uint16_t* __restrict__ g, uint16_t* __restrict__ w, int64_t ntiles, int64_t tail,
+               const void* __restrict__ gv, uint16_t* __restrict__ w, int64_t ntiles, int64_t tail,
                dos_kscal s, dos_peers pr, int l2ef) {
   constexpr int TE = 4 * NT;  // 4 elements per thread per tile
-  constexpr uint32_t F32B = TE * 4, H16B = TE * 2, STAGE = 3 * F32B + H16B;
+  constexpr uint32_t F32B = TE * 4, H16B = TE * 2, GB = GT == DOS_F32 ? F32B : H16B;
+  constexpr uint32_t STAGE = tma_stage_bytes<GT, LT, NT>();
+  constexpr uint32_t WOFF = GT == DOS_F32 ? 3 * F32B + GB : 3 * F32B;  // working-copy slot
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t full[S];
   const int tid = threadIdx.x;
   const int64_t first = blockIdx.x, step = gridDim.x;
   const int64_t mine = ntiles > first ? (ntiles - first + step - 1) / step : 0;
   const uint64_t pol = l2ef ? l2_evict_first() : 0;
+  const char* g = static_cast<const char*>(gv);
+  constexpr int GE = GT == DOS_F32 ? 4 : 2;  // bytes per grad element
 
-  auto stage_ptr = [&](int st, int piece) -> unsigned char* { return smem + st * STAGE + piece * F32B; };
+  auto stage_ptr = [&](int st, int piece) -> unsigned char* {
+    return smem + st * STAGE + (piece == 4 ? WOFF : piece * F32B);
+  };
   auto load = [&](void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     if (l2ef) bulk_load_ef(dst, src, bytes, bar, pol);
     else bulk_load(dst, src, bytes, bar);
@@ -335,7 +349,7 @@ __global__ void __launch_bounds__(NT, 1)
     load(stage_ptr(st, 0), p + e0, F32B, &full[st]);
     load(stage_ptr(st, 1), m + e0, F32B, &full[st]);
     load(stage_ptr(st, 2), v + e0, F32B, &full[st]);
-    load(stage_ptr(st, 3), g + e0, H16B, &full[st]);
+    load(stage_ptr(st, 3), g + e0 * GE, GB, &full[st]);
   };
 
   if (tid == 0) {
@@ -353,24 +367,29 @@ __global__ void __launch_bounds__(NT, 1)
     float4* P = reinterpret_cast<float4*>(stage_ptr(st, 0)) + tid;
     float4* M = reinterpret_cast<float4*>(stage_ptr(st, 1)) + tid;
     float4* V = reinterpret_cast<float4*>(stage_ptr(st, 2)) + tid;
-    uint2* G = reinterpret_cast<uint2*>(stage_ptr(st, 3)) + tid;
     float4 pp = *P, mm = *M, vv = *V;
-    const uint2 gg = *G;
     float pe[4] = {pp.x, pp.y, pp.z, pp.w}, me[4] = {mm.x, mm.y, mm.z, mm.w}, ve[4] = {vv.x, vv.y, vv.z, vv.w};
-    const uint16_t gb[4] = {(uint16_t)(gg.x & 0xffffu), (uint16_t)(gg.x >> 16), (uint16_t)(gg.y & 0xffffu),
-                            (uint16_t)(gg.y >> 16)};
+    float ge[4];
+    if (GT == DOS_F32) {
+      const float4 gg = reinterpret_cast<const float4*>(stage_ptr(st, 3))[tid];
+      ge[0] = gg.x; ge[1] = gg.y; ge[2] = gg.z; ge[3] = gg.w;
+    } else {
+      const uint2 gg = reinterpret_cast<const uint2*>(stage_ptr(st, 3))[tid];
+      const uint16_t gb[4] = {(uint16_t)(gg.x & 0xffffu), (uint16_t)(gg.x >> 16), (uint16_t)(gg.y & 0xffffu),
+                              (uint16_t)(gg.y >> 16)};
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float gj = GT == DOS_BF16 ? dos_bf16_to_f32(gb[j]) : __half2float(__ushort_as_half(gb[j]));
-      dos_adam_elem(pe[j], me[j], ve[j], gj, s);
+      for (int j = 0; j < 4; ++j)
+        ge[j] = GT == DOS_BF16 ? dos_bf16_to_f32(gb[j]) : __half2float(__ushort_as_half(gb[j]));
     }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) dos_adam_elem(pe[j], me[j], ve[j], ge[j], s);
     *P = make_float4(pe[0], pe[1], pe[2], pe[3]);
     *M = make_float4(me[0], me[1], me[2], me[3]);
     *V = make_float4(ve[0], ve[1], ve[2], ve[3]);
     if (LT != DOS_NONE) {
       const uint2 wv = make_uint2((uint32_t)to_lowp(pe[0], LT) | ((uint32_t)to_lowp(pe[1], LT) << 16),
                                   (uint32_t)to_lowp(pe[2], LT) | ((uint32_t)to_lowp(pe[3], LT) << 16));
-      *G = wv;
+      reinterpret_cast<uint2*>(stage_ptr(st, 4))[tid] = wv;
       // fused all-gather: the same 8 bytes straight into every peer's copy
       // (NVLink stores through IPC-mapped addresses), coalesced per warp
       const int64_t e0 = (first + k * step) * TE;
@@ -383,7 +402,7 @@ __global__ void __launch_bounds__(NT, 1)
       store(p + e0, stage_ptr(st, 0), F32B);
       store(m + e0, stage_ptr(st, 1), F32B);
       store(v + e0, stage_ptr(st, 2), F32B);
-      if (LT != DOS_NONE) store(w + e0, stage_ptr(st, 3), H16B);
+      if (LT != DOS_NONE) store(w + e0, stage_ptr(st, 4), H16B);
       bulk_commit();
       if (k + S - 1 < mine) {
         bulk_wait_read<1>();  // the refilled stage's stores (tile k-1) have left shared memory
@@ -398,7 +417,7 @@ __global__ void __launch_bounds__(NT, 1)
     for (int64_t j = tid; j < tail; j += NT) {
       const int64_t e = base + j;
       float pe = p[e], me = m[e], ve = v[e];
-      const float gj = GT == DOS_BF16 ? dos_bf16_to_f32(g[e]) : __half2float(__ushort_as_half(g[e]));
+      const float gj = load_g1(gv, GT, e);
       dos_adam_elem(pe, me, ve, gj, s);
       p[e] = pe;
       m[e] = me;
@@ -414,9 +433,9 @@ __global__ void __launch_bounds__(NT, 1)
 }
 
 template <int GT, int LT, int NT, int S>
-int launch_tma_cfg(float* p, float* m, float* v, const uint16_t* g, uint16_t* w, int64_t ntiles, int64_t tail,
+int launch_tma_cfg(float* p, float* m, float* v, const void* g, uint16_t* w, int64_t ntiles, int64_t tail,
                    const dos_kscal& s, int ctas_per_sm, cudaStream_t st, const dos_peers& pr) {
-  constexpr int smem = S * 4 * NT * 14;
+  constexpr int smem = S * tma_stage_bytes<GT, LT, NT>();
   static bool configured = false;
   if (!configured) {
     const cudaError_t e =
@@ -467,8 +486,15 @@ bool tma_enabled() {
   return on == 1;
 }
 
+// Does the selected pipeline shape fit in a CTA's shared memory for these dtypes?
+bool tma_fits(int gt, int lt) {
+  const TmaCfg& c = tma_cfg();
+  const int per_elem = 12 + (gt == DOS_F32 ? 4 : 2) + ((gt == DOS_F32 && lt != DOS_NONE) ? 2 : 0);
+  return (int64_t)c.stages * 4 * c.nt * per_elem <= 227 * 1024;
+}
+
 template <int GT, int LT>
-int launch_adam_tma(float* p, float* m, float* v, const uint16_t* g, uint16_t* w, int64_t ntiles, int64_t tail,
+int launch_adam_tma(float* p, float* m, float* v, const void* g, uint16_t* w, int64_t ntiles, int64_t tail,
                     const dos_kscal& s, cudaStream_t st, const dos_peers& pr) {
   const TmaCfg& c = tma_cfg();
 #define DOS_CFG(NT_, S_) \
@@ -523,9 +549,10 @@ int dos_adam_launch(float* p, float* m, float* v, const void* g, int gt, void* l
     eb[5 + r] = 2;
   }
   int64_t head = common_head(ptrs, eb, lt == DOS_NONE ? 4 : 5 + pr.n, n);
-  // TMA path: 16-bit grads, a 16-byte-alignable range of at least one tile.
-  if (gt != DOS_F32 && (lt == DOS_NONE || lt == DOS_F16 || lt == DOS_BF16) && head >= 0 && tma_enabled() &&
-      (n - head) / (4 * tma_cfg().nt) >= 1) {
+  // TMA path: a 16-byte-alignable range of at least one tile whose pipeline
+  // shape fits in shared memory (all grad dtypes).
+  if ((gt == DOS_F32 || gt == DOS_F16 || gt == DOS_BF16) && (lt == DOS_NONE || lt == DOS_F16 || lt == DOS_BF16) &&
+      head >= 0 && tma_enabled() && tma_fits(gt, lt) && (n - head) / (4 * tma_cfg().nt) >= 1) {
     const int64_t tile = 4 * tma_cfg().nt;
     const int64_t ntiles = (n - head) / tile;
     const int64_t tail = n - head - ntiles * tile;  // < one tile; handled inside the same launch
@@ -534,13 +561,14 @@ int dos_adam_launch(float* p, float* m, float* v, const void* g, int gt, void* l
     int rc = DOS_OK;
     if (head > 0) rc = dos_adam_launch(p, m, v, g, gt, lp, lt, head, s, st, pr);  // < 8 elements: register path
     if (rc != DOS_OK) return rc;
-    const uint16_t* gb = reinterpret_cast<const uint16_t*>(gc + 2 * head);
+    const void* gb = gc + (gt == DOS_F32 ? 4 : 2) * head;
     uint16_t* wb = lt == DOS_NONE ? nullptr : reinterpret_cast<uint16_t*>(lc + 2 * head);
     const dos_peers pb = dos_peers_offset(pr, head);
 #define DOS_TMA(G, L) \
   if (gt == G && lt == L) rc = launch_adam_tma<G, L>(p + head, m + head, v + head, gb, wb, ntiles, tail, s, st, pb);
     DOS_TMA(DOS_F16, DOS_NONE) else DOS_TMA(DOS_F16, DOS_F16) else DOS_TMA(DOS_F16, DOS_BF16)
     else DOS_TMA(DOS_BF16, DOS_NONE) else DOS_TMA(DOS_BF16, DOS_F16) else DOS_TMA(DOS_BF16, DOS_BF16)
+    else DOS_TMA(DOS_F32, DOS_NONE) else DOS_TMA(DOS_F32, DOS_F16) else DOS_TMA(DOS_F32, DOS_BF16)
 #undef DOS_TMA
     if (rc != DOS_OK) return rc;
     cudaError_t e = cudaGetLastError();
