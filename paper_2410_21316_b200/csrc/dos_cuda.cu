@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(NT, 1)
   auto issue = [&](int64_t k) {  // tile k of this CTA into stage k % S
     const int st = (int)(k % S);
     const int64_t e0 = (first + k * step) * TE;
-    mbar_expect_tx(&full[st], STAGE);
+    mbar_expect_tx(&full[st], 3 * F32B + GB);  // the bytes the four loads deliver (not the W slot)
     load(stage_ptr(st, 0), p + e0, F32B, &full[st]);
     load(stage_ptr(st, 1), m + e0, F32B, &full[st]);
     load(stage_ptr(st, 2), v + e0, F32B, &full[st]);
