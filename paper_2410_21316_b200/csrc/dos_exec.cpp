@@ -69,6 +69,7 @@ struct Engine {
   cudaStream_t st[3] = {nullptr, nullptr, nullptr};  // fast, h2d, d2h
   cudaStream_t gst = nullptr;                        // in-phase grad flush (D2H)
   std::vector<cudaEvent_t> ev_g;                      // per action: its grads are on the host
+  std::vector<cudaEvent_t> ev_sg;                     // per subgroup: host_io grads of a static resident landed
   int nslots = 0;
   int64_t slot_elems = 0;
   float* slot_mem = nullptr;
@@ -334,7 +335,8 @@ struct Engine {
         if (a->is_static) {
           const int64_t o = static_off[sg];
           if (o < 0) return dos_set_error(DOS_ESTATE, "subgroup %d marked static but has no HBM residence", sg);
-          if (S.host_io) DOS_CU(copy_grads_h2d(start, n, s));
+          // host_io: its grads were shipped H2D at phase start on the side stream
+          if (S.host_io) DOS_CU(cudaStreamWaitEvent(s, ev_sg[sg], 0));
           return dos_adam_launch(S.dev_static_p + o, S.dev_static_m + o, S.dev_static_v + o, g, lt, lp, lt, n, K, s,
                                  dos_peers_offset(peers, start));
         }
@@ -349,7 +351,12 @@ struct Engine {
         // K1 already stored the working copy in the same pass.
         if (!a->is_static && !(sg_slot[sg] >= 0 && (sg_mask[sg] & (1u << PIECE_P))))
           return dos_set_error(DOS_ESTATE, "FLUSH_OUT_MODEL16 of subgroup %d without staged params", sg);
-        if (S.host_io && a->is_static) DOS_CU(copy_lowp_d2h(start, n, s));
+        if (S.host_io && a->is_static) {
+          // mirror a resident's working copy on the side stream, off the compute lane
+          DOS_CU(cudaEventRecord(ev_sg[sg], s));
+          DOS_CU(cudaStreamWaitEvent(gst, ev_sg[sg], 0));
+          DOS_CU(copy_lowp_d2h(start, n, gst));
+        }
         return DOS_OK;
       case DOS_FLUSH_OUT_M:
       case DOS_FLUSH_OUT_V:
@@ -444,6 +451,20 @@ struct Engine {
     DOS_CU(cudaStreamWaitEvent(st[1], ev0, 0));
     DOS_CU(cudaStreamWaitEvent(st[2], ev0, 0));
     DOS_CU(cudaStreamWaitEvent(gst, ev0, 0));
+    if (S.host_io) {
+      // static residents' grads go H2D first thing, on the side stream, so
+      // their updates (STATIC_LAST: at the end of the phase) never wait on them
+      while ((int)ev_sg.size() < ns) {
+        cudaEvent_t e;
+        DOS_CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ev_sg.push_back(e);
+      }
+      for (int i = 0; i < ns; ++i)
+        if (static_off[i] >= 0) {
+          DOS_CU(copy_grads_h2d(sg_start[i], sg_size[i], gst));
+          DOS_CU(cudaEventRecord(ev_sg[i], gst));
+        }
+    }
     DOS_CU(cudaEventSynchronize(ev0));
     host_t0 = now_ns();
     active = true;
@@ -528,6 +549,7 @@ struct Engine {
     for (auto e : ev_s) cudaEventDestroy(e);
     for (auto e : ev_e) cudaEventDestroy(e);
     for (auto e : ev_g) cudaEventDestroy(e);
+    for (auto e : ev_sg) cudaEventDestroy(e);
     if (ev0) cudaEventDestroy(ev0);
     if (slot_mem) cudaFree(slot_mem);
     if (flags) cudaFreeHost(flags);
