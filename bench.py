@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--host-threads", type=int, default=0, help="H1 team size (0: all allowed cores / ranks)")
     ap.add_argument("--trace-dir", default=None, help="write measured/predicted timelines as trace CSVs")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N>1 (gloo: dry run with ranks sharing GPUs)")
     ap.add_argument("--no-ref-schedule", action="store_true",
                     help="skip timing the reference's ALL_CPU offload schedule on this runtime")
     ap.add_argument("--static-variants", default="0.0,0.5,1.0",
@@ -219,10 +221,16 @@ class B200Bench:
 
         self.args, self.rank, self.world = args, rank, world
         self.torch, self.dist, self.D, self.policy, self.profile_b200 = torch, dist, D, policy, profile_b200
-        torch.cuda.set_device(local)
-        self.device = torch.device("cuda", local)
+        # --dist-backend gloo lets several ranks share fewer GPUs (a dry run of the
+        # multi-rank path on a one-GPU box); the product path is NCCL, one GPU per rank
+        dev_index = local % max(1, torch.cuda.device_count()) if args.dist_backend == "gloo" else local
+        torch.cuda.set_device(dev_index)
+        self.device = torch.device("cuda", dev_index)
         if world > 1:
-            dist.init_process_group("nccl", device_id=self.device)
+            if args.dist_backend == "nccl":
+                dist.init_process_group("nccl", device_id=self.device)
+            else:
+                dist.init_process_group("gloo")
             D._native.lib().dos_set_host_threads(max(1, len(os.sched_getaffinity(0)) // world))
         if args.host_threads > 0:
             D._native.lib().dos_set_host_threads(args.host_threads)
@@ -238,7 +246,8 @@ class B200Bench:
     def max_over_ranks(self, x: float) -> float:
         if self.world == 1:
             return x
-        t = self.torch.tensor([x], dtype=self.torch.float64, device=self.device)
+        t = self.torch.tensor([x], dtype=self.torch.float64,
+                              device=self.device if self.args.dist_backend == "nccl" else "cpu")
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
