@@ -81,6 +81,24 @@ int dos_adam_step_cuda_bcast(float* p, float* m, float* v, const void* g, int g_
                              void* p_lowp, int lowp_dtype, void* const* peer_lowp, int npeers,
                              int64_t n, const dos_adam_scalars* s, void* stream);
 
+/* K1 with the reduce-scatter fused into its grad load (and, optionally, the
+ * all-gather into its epilogue): g_src[r] (r < nsrc <= DOS_MAX_PEERS + 1, in
+ * rank order) holds rank r's grads for this range; g_src[self] is local and
+ * streamed by TMA, the others are loaded over NVLink one tile ahead.  The
+ * grads used are lowp(rank-order fp32 sum) [then lowp(x * grad_scale) if
+ * grad_scale != 1]; 16-bit grads only, working copy in the same dtype.
+ * Replaces the bucketed NCCL reduce-scatter before the phase. */
+int dos_adam_step_cuda_rs(float* p, float* m, float* v, const void* const* g_src, int nsrc, int self,
+                          int g_dtype, float grad_scale, void* p_lowp, int lowp_dtype,
+                          void* const* peer_lowp, int npeers, int64_t n, const dos_adam_scalars* s,
+                          void* stream);
+
+/* Stand-alone reduce-scatter of one range with the same rounding:
+ * out[i] = lowp(sum_r src[r][i]) (scaled as above); out may alias a source
+ * (in place).  Used for the host subgroups' grads before their D2H flush. */
+int dos_reduce_scatter_cuda(void* out, const void* const* src, int nsrc, int dtype, float scale,
+                            int64_t n, void* stream);
+
 /* ---- CUDA IPC for symmetric full-model buffers (one process per GPU).
  * export: the handle of the allocation containing dev_ptr and dev_ptr's
  * byte offset in it; import: map a peer's allocation (cached) and return
@@ -168,6 +186,22 @@ typedef struct dos_state_desc {
    * (pinned DMA, in subgroup order, on a dedicated stream) and the host lane
    * waits only for its own subgroup's copy; the upcast is fused into H1. */
   int32_t flush_grads;
+  /* Fused reduce-scatter of the grads (ZeRO-3, one node), replacing the
+   * bucketed NCCL reduce-scatter before the phase.  nsrc_g = world size
+   * (0 = off); src_g[r] is where THIS rank's shard starts inside rank r's
+   * full-model grad buffer (r in rank order; src_g[self_rank] must be
+   * dev_g — peers are IPC-mapped NVLink addresses).  A subgroup's grads are
+   * lowp(fp32 sum over r in rank order), then lowp(that * grad_scale) when
+   * grad_scale != 1.  GPU_UPDATE reduces inside K1 (peer loads over NVLink);
+   * a CPU_UPDATE's grads are reduced into dev_g on the grad stream right
+   * before their in-phase flush, so nsrc_g > 0 requires flush_grads and
+   * excludes host_io.  Every rank must have finished writing its grads before
+   * the phase starts, and none may overwrite them until every rank's phase
+   * has ended (the caller's barriers). */
+  int32_t nsrc_g;
+  int32_t self_rank;
+  const void* const* src_g;
+  float grad_scale;
 } dos_state_desc;
 
 #define DOS_MAX_PEERS 7

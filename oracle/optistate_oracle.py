@@ -72,6 +72,23 @@ def f32_from_lowp(x, lowp):
     return f32_from_f16(x) if lowp == "fp16" else f32_from_bf16(x)
 
 
+def reduce_scatter(sources, lowp, scale=1.0):
+    """The ZeRO-3 grad reduce-scatter for one rank's shard, as the fused
+    B200 path defines it (include/dos.h, dos_state_desc.src_g).  NOT pinned by
+    the reference, which has no collectives:
+    declared order — widen every rank's grads exactly (core.py:201-205), sum
+    in fp32 in rank order with one RN rounding per add, round once to the
+    grad dtype (RNE), then, if scale != 1, round(f32(x) * f32(scale)) again.
+    ``sources`` are the ranks' half-precision arrays in rank order."""
+    acc = f32_from_lowp(sources[0], lowp).astype(np.float32, copy=True)
+    for src in sources[1:]:
+        acc = np.add(acc, f32_from_lowp(src, lowp), dtype=np.float32)
+    out = lowp_from_f32(acc, lowp)
+    if scale != 1.0:
+        out = lowp_from_f32(np.multiply(f32_from_lowp(out, lowp), np.float32(scale), dtype=np.float32), lowp)
+    return out
+
+
 def shard_subgroups(total: int, subgroup_size: int):
     """core.py:139-170 for one rank: (start, size) per subgroup."""
     return [(s, min(subgroup_size, total - s)) for s in range(0, total, subgroup_size)]

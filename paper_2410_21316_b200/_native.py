@@ -58,6 +58,10 @@ class dos_state_desc(C.Structure):
         ("npeers", C.c_int32),
         ("peer_lowp", C.POINTER(C.c_void_p)),
         ("flush_grads", C.c_int32),
+        ("nsrc_g", C.c_int32),
+        ("self_rank", C.c_int32),
+        ("src_g", C.POINTER(C.c_void_p)),
+        ("grad_scale", C.c_float),
     ]
 
 
@@ -89,6 +93,9 @@ SIGNATURES: dict[str, tuple] = {
     "dos_adam_step_host": (_I, [_VP, _VP, _VP, _VP, _I, _VP, _I, _I64, C.POINTER(dos_adam_scalars), _I]),
     "dos_adam_step_cuda_bcast": (_I, [_VP, _VP, _VP, _VP, _I, _VP, _I, C.POINTER(_VP), _I, _I64,
                                       C.POINTER(dos_adam_scalars), _VP]),
+    "dos_adam_step_cuda_rs": (_I, [_VP, _VP, _VP, C.POINTER(_VP), _I, _I, _I, C.c_float, _VP, _I, C.POINTER(_VP),
+                                   _I, _I64, C.POINTER(dos_adam_scalars), _VP]),
+    "dos_reduce_scatter_cuda": (_I, [_VP, C.POINTER(_VP), _I, _I, C.c_float, _I64, _VP]),
     "dos_ipc_export": (_I, [_VP, C.c_char_p, C.POINTER(C.c_uint64)]),
     "dos_ipc_import": (_I, [C.c_char_p, C.c_uint64, C.POINTER(_VP)]),
     "dos_ipc_close_all": (_I, []),

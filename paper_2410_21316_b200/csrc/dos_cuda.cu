@@ -65,13 +65,51 @@ __device__ __forceinline__ uint16_t to_lowp(float x, int lt) {
   return lt == DOS_BF16 ? dos_f32_to_bf16(x) : dos_f32_to_f16(x);
 }
 
+__device__ __forceinline__ float widen16(uint16_t b, int gt) {
+  return gt == DOS_BF16 ? dos_bf16_to_f32(b) : __half2float(__ushort_as_half(b));  // exact
+}
+
+// The fused reduce-scatter's rounding (dos_gsrc): the fp32 rank-order sum
+// rounded to the grad dtype, then the optional averaging scale, rounded again.
+__device__ __forceinline__ float rs_round(float acc, int gt, float scale) {
+  uint16_t b = to_lowp(acc, gt);
+  if (scale != 1.0f) b = to_lowp(__fmul_rn(widen16(b, gt), scale), gt);
+  return widen16(b, gt);
+}
+
+// Reduced grad of element e (scalar path).
+__device__ __forceinline__ float rs_reduce1(const dos_gsrc& gs, int gt, int64_t e) {
+  float acc = widen16(gs.p[0][e], gt);
+  for (int r = 1; r < gs.n; ++r) acc = __fadd_rn(acc, widen16(gs.p[r][e], gt));
+  return rs_round(acc, gt, gs.scale);
+}
+
+// Reduced grads of the 8 elements at base + 8*i (16-byte loads; base + 8*i
+// is 16-byte aligned in every source).
+__device__ __forceinline__ void rs_reduce8(const dos_gsrc& gs, int gt, int64_t base, int64_t i, float* out) {
+#pragma unroll
+  for (int r = 0; r < DOS_MAX_PEERS + 1; ++r) {
+    if (r >= gs.n) break;
+    const uint4 w = __ldcs(reinterpret_cast<const uint4*>(gs.p[r] + base) + i);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float lo = widen16((uint16_t)(ws[k] & 0xffffu), gt), hi = widen16((uint16_t)(ws[k] >> 16), gt);
+      out[2 * k] = r ? __fadd_rn(out[2 * k], lo) : lo;
+      out[2 * k + 1] = r ? __fadd_rn(out[2 * k + 1], hi) : hi;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) out[k] = rs_round(out[k], gt, gs.scale);
+}
+
 // Vector body over [base, base + 8*nvec), plus `nscalar` scalar elements
 // (the unaligned head [0, head) and the tail after the vector body).
 template <int GT, int LT>
 __global__ void __launch_bounds__(kThreads)
     k_adam(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
-           const void* __restrict__ g, void* __restrict__ lp, int64_t head, int64_t nvec,
-           int64_t n, dos_kscal s, dos_peers pr) {
+           const void* g, void* __restrict__ lp, int64_t head, int64_t nvec,
+           int64_t n, dos_kscal s, dos_peers pr, dos_gsrc gs) {
   const int64_t tid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   const int64_t nthr = (int64_t)gridDim.x * kThreads;
 
@@ -89,7 +127,15 @@ __global__ void __launch_bounds__(kThreads)
     const float4 m0 = __ldcs(M), m1 = __ldcs(M + 1);
     const float4 v0 = __ldcs(V), v1 = __ldcs(V + 1);
     float gg[kVec];
-    load_g8(gv, GT, i, gg);
+    if (GT != DOS_F32 && gs.n > 0) {  // fused reduce-scatter; the reduced grads replace the local ones
+      rs_reduce8(gs, GT, head, i, gg);
+      uint32_t rw[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) rw[k] = (uint32_t)to_lowp(gg[2 * k], GT) | ((uint32_t)to_lowp(gg[2 * k + 1], GT) << 16);
+      __stcs(reinterpret_cast<uint4*>(const_cast<char*>(gv)) + i, make_uint4(rw[0], rw[1], rw[2], rw[3]));
+    } else {
+      load_g8(gv, GT, i, gg);
+    }
     float pe[kVec] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
     float me[kVec] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
     float ve[kVec] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
@@ -118,7 +164,14 @@ __global__ void __launch_bounds__(kThreads)
   for (int64_t j = tid; j < nscalar; j += nthr) {
     const int64_t e = j < head ? j : vec_end + (j - head);
     float pe = p[e], me = m[e], ve = v[e];
-    dos_adam_elem(pe, me, ve, load_g1(g, GT, e), s);
+    float ge;
+    if (GT != DOS_F32 && gs.n > 0) {
+      ge = rs_reduce1(gs, GT, e);
+      reinterpret_cast<uint16_t*>(const_cast<void*>(g))[e] = to_lowp(ge, GT);
+    } else {
+      ge = load_g1(g, GT, e);
+    }
+    dos_adam_elem(pe, me, ve, ge, s);
     p[e] = pe;
     m[e] = me;
     v[e] = ve;
@@ -149,6 +202,30 @@ __global__ void __launch_bounds__(kThreads)
   for (int64_t j = tid; j < nscalar; j += nthr) {
     const int64_t e = j < head ? j : vec_end + (j - head);
     o[e] = to_lowp(x[e], OT);
+  }
+}
+
+// Stand-alone reduce-scatter of a range (dos_gsrc rounding): the rank-order
+// fp32 sum of every source, rounded to the 16-bit dtype.  Reads 2 B/param
+// per rank (all but one over NVLink), writes 2 B/param.
+template <int DT>
+__global__ void __launch_bounds__(kThreads)
+    k_reduce(uint16_t* __restrict__ o, int64_t head, int64_t nvec, int64_t n, dos_gsrc gs) {
+  const int64_t tid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  const int64_t nthr = (int64_t)gridDim.x * kThreads;
+  for (int64_t i = tid; i < nvec; i += nthr) {
+    float e[8];
+    rs_reduce8(gs, DT, head, i, e);
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) w[k] = (uint32_t)to_lowp(e[2 * k], DT) | ((uint32_t)to_lowp(e[2 * k + 1], DT) << 16);
+    __stcs(reinterpret_cast<uint4*>(o + head) + i, make_uint4(w[0], w[1], w[2], w[3]));
+  }
+  const int64_t vec_end = head + kVec * nvec;
+  const int64_t nscalar = head + (n - vec_end);
+  for (int64_t j = tid; j < nscalar; j += nthr) {
+    const int64_t e = j < head ? j : vec_end + (j - head);
+    o[e] = to_lowp(rs_reduce1(gs, DT, e), DT);
   }
 }
 
@@ -216,7 +293,7 @@ unsigned grid_for(int64_t work) {
 
 template <int GT, int LT>
 void launch_adam(float* p, float* m, float* v, const void* g, void* lp, int64_t head, int64_t nvec,
-                 int64_t n, const dos_kscal& s, cudaStream_t st, const dos_peers& pr) {
+                 int64_t n, const dos_kscal& s, cudaStream_t st, const dos_peers& pr, const dos_gsrc& gs) {
   const int64_t work = nvec > 0 ? nvec : n;
   static int cap_blocks = 0;  // resident CTAs per SM for this instantiation
   if (!cap_blocks) {
@@ -227,7 +304,7 @@ void launch_adam(float* p, float* m, float* v, const void* g, void* lp, int64_t 
   const int64_t cap = (int64_t)sm_count() * cap_blocks;
   int64_t want = (work + kThreads - 1) / kThreads;
   want = want < 1 ? 1 : (want < cap ? want : cap);
-  k_adam<GT, LT><<<(unsigned)want, kThreads, 0, st>>>(p, m, v, g, lp, head, nvec, n, s, pr);
+  k_adam<GT, LT><<<(unsigned)want, kThreads, 0, st>>>(p, m, v, g, lp, head, nvec, n, s, pr, gs);
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
@@ -322,11 +399,16 @@ __host__ __device__ constexpr uint32_t tma_stage_bytes() {
   return 4 * NT * (12 + (GT == DOS_F32 ? 4 : 2) + ((GT == DOS_F32 && LT != DOS_NONE) ? 2 : 0));
 }
 
-template <int GT, int LT, int NT, int S>
+// RS: the grads are the fused reduce-scatter of gs (16-bit grads only).  The
+// local rank's tile still arrives by TMA; every other rank's 4 elements of
+// this thread come over NVLink as one 8-byte load per rank, issued one tile
+// ahead (right after the current tile's are consumed) so their latency hides
+// behind this tile's update, stores and the next stage wait.
+template <int GT, int LT, int NT, int S, bool RS = false>
 __global__ void __launch_bounds__(NT, 1)
     k_adam_tma(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
-               const void* __restrict__ gv, uint16_t* __restrict__ w, int64_t ntiles, int64_t tail,
-               dos_kscal s, dos_peers pr, int l2ef) {
+               const void* gv, uint16_t* __restrict__ w, int64_t ntiles, int64_t tail,
+               dos_kscal s, dos_peers pr, int l2ef, dos_gsrc gs) {
   constexpr int TE = 4 * NT;  // 4 elements per thread per tile
   constexpr uint32_t F32B = TE * 4, H16B = TE * 2, GB = GT == DOS_F32 ? F32B : H16B;
   constexpr uint32_t STAGE = tma_stage_bytes<GT, LT, NT>();
@@ -370,6 +452,15 @@ __global__ void __launch_bounds__(NT, 1)
   if (tid == 0)
     for (int64_t k = 0; k < S - 1 && k < mine; ++k) issue(k);
 
+  uint2 nx[RS ? DOS_MAX_PEERS + 1 : 1];  // the other ranks' grads of the next tile (RS)
+  auto rs_fetch = [&](int64_t k) {
+    const int64_t e0 = (first + k * step) * TE;
+#pragma unroll
+    for (int r = 0; r < (RS ? DOS_MAX_PEERS + 1 : 0); ++r)
+      if (r < gs.n && r != gs.self) nx[r] = __ldcs(reinterpret_cast<const uint2*>(gs.p[r] + e0) + tid);
+  };
+  if (RS && mine > 0) rs_fetch(0);
+
   for (int64_t k = 0; k < mine; ++k) {
     const int st = (int)(k % S);
     mbar_wait(&full[st], (uint32_t)((k / S) & 1));
@@ -389,6 +480,32 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         ge[j] = GT == DOS_BF16 ? dos_bf16_to_f32(gb[j]) : __half2float(__ushort_as_half(gb[j]));
+      if (RS) {  // rank-order fp32 sum with the local tile at position gs.self
+        float acc[4];
+#pragma unroll
+        for (int r = 0; r < DOS_MAX_PEERS + 1; ++r) {
+          if (r >= gs.n) break;
+          float x[4];
+          if (r == gs.self) {
+            x[0] = ge[0]; x[1] = ge[1]; x[2] = ge[2]; x[3] = ge[3];
+          } else {
+            x[0] = widen16((uint16_t)(nx[r].x & 0xffffu), GT);
+            x[1] = widen16((uint16_t)(nx[r].x >> 16), GT);
+            x[2] = widen16((uint16_t)(nx[r].y & 0xffffu), GT);
+            x[3] = widen16((uint16_t)(nx[r].y >> 16), GT);
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[j] = r ? __fadd_rn(acc[j], x[j]) : x[j];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ge[j] = rs_round(acc[j], GT, gs.scale);
+        if (k + 1 < mine) rs_fetch(k + 1);
+        // the reduced grads replace the local ones (as an NCCL reduce-scatter would leave them)
+        const int64_t e0 = (first + k * step) * TE;
+        __stcs(reinterpret_cast<uint2*>(const_cast<char*>(g) + e0 * GE) + tid,
+               make_uint2((uint32_t)to_lowp(ge[0], GT) | ((uint32_t)to_lowp(ge[1], GT) << 16),
+                          (uint32_t)to_lowp(ge[2], GT) | ((uint32_t)to_lowp(ge[3], GT) << 16)));
+      }
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) dos_adam_elem(pe[j], me[j], ve[j], ge[j], s);
@@ -426,7 +543,8 @@ __global__ void __launch_bounds__(NT, 1)
     for (int64_t j = tid; j < tail; j += NT) {
       const int64_t e = base + j;
       float pe = p[e], me = m[e], ve = v[e];
-      const float gj = load_g1(gv, GT, e);
+      const float gj = RS ? rs_reduce1(gs, GT, e) : load_g1(gv, GT, e);
+      if (RS) reinterpret_cast<uint16_t*>(const_cast<void*>(gv))[e] = to_lowp(gj, GT);
       dos_adam_elem(pe, me, ve, gj, s);
       p[e] = pe;
       m[e] = me;
@@ -441,14 +559,15 @@ __global__ void __launch_bounds__(NT, 1)
   if (tid == 0) bulk_wait_all();
 }
 
-template <int GT, int LT, int NT, int S>
+template <int GT, int LT, int NT, int S, bool RS = false>
 int launch_tma_cfg(float* p, float* m, float* v, const void* g, uint16_t* w, int64_t ntiles, int64_t tail,
-                   const dos_kscal& s, int ctas_per_sm, cudaStream_t st, const dos_peers& pr) {
+                   const dos_kscal& s, int ctas_per_sm, cudaStream_t st, const dos_peers& pr,
+                   const dos_gsrc& gs = dos_gsrc{0, 0, 1.0f, {}}) {
   constexpr int smem = S * tma_stage_bytes<GT, LT, NT>();
   static bool configured = false;
   if (!configured) {
     const cudaError_t e =
-        cudaFuncSetAttribute(k_adam_tma<GT, LT, NT, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_adam_tma<GT, LT, NT, S, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return dos_set_error(DOS_ECUDA, "K1 smem attribute: %s", cudaGetErrorString(e));
     configured = true;
   }
@@ -460,7 +579,7 @@ int launch_tma_cfg(float* p, float* m, float* v, const void* g, uint16_t* w, int
     const char* e = getenv("DOS_K1_L2");
     return (e && strcmp(e, "evict_first") == 0) ? 1 : 0;
   }();
-  k_adam_tma<GT, LT, NT, S><<<(unsigned)grid, NT, smem, st>>>(p, m, v, g, w, ntiles, tail, s, pr, l2ef);
+  k_adam_tma<GT, LT, NT, S, RS><<<(unsigned)grid, NT, smem, st>>>(p, m, v, g, w, ntiles, tail, s, pr, l2ef, gs);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return DOS_OK;
 }
@@ -547,32 +666,76 @@ dos_peers dos_peers_offset(const dos_peers& pr, int64_t elems) {
   return o;
 }
 
+dos_gsrc dos_gsrc_offset(const dos_gsrc& gs, int64_t elems) {
+  dos_gsrc o = gs;
+  for (int r = 0; r < gs.n; ++r) o.p[r] = gs.p[r] + elems;
+  return o;
+}
+
 int dos_adam_launch(float* p, float* m, float* v, const void* g, int gt, void* lp, int lt, int64_t n,
-                    const dos_kscal& s, cudaStream_t st, const dos_peers& pr) {
+                    const dos_kscal& s, cudaStream_t st, const dos_peers& pr, const dos_gsrc& gs) {
   if (n == 0) return DOS_OK;
   if (pr.n > 0 && lt == DOS_NONE) return dos_set_error(DOS_EINVAL, "peer broadcast needs a working-copy dtype");
-  const void* ptrs[5 + DOS_MAX_PEERS] = {p, m, v, g, lp};
-  int eb[5 + DOS_MAX_PEERS] = {4, 4, 4, gt == DOS_F32 ? 4 : 2, 2};
-  for (int r = 0; r < pr.n; ++r) {  // peers share the 16-byte phase of the local stores
-    ptrs[5 + r] = pr.p[r];
-    eb[5 + r] = 2;
+  if (gs.n > 0 && gt == DOS_F32) return dos_set_error(DOS_ETYPE, "the fused reduce-scatter takes 16-bit grads");
+  const void* ptrs[5 + 2 * DOS_MAX_PEERS + 1] = {p, m, v, g, lp};
+  int eb[5 + 2 * DOS_MAX_PEERS + 1] = {4, 4, 4, gt == DOS_F32 ? 4 : 2, 2};
+  int k = 5;
+  for (int r = 0; r < pr.n; ++r, ++k) {  // peers share the 16-byte phase of the local stores
+    ptrs[k] = pr.p[r];
+    eb[k] = 2;
   }
-  int64_t head = common_head(ptrs, eb, lt == DOS_NONE ? 4 : 5 + pr.n, n);
+  for (int r = 0; r < gs.n; ++r, ++k) {  // and so do the reduce-scatter's sources
+    ptrs[k] = gs.p[r];
+    eb[k] = 2;
+  }
+  if (lt == DOS_NONE) {  // no working copy: drop lp from the alignment set
+    for (int j = 4; j + 1 < k; ++j) {
+      ptrs[j] = ptrs[j + 1];
+      eb[j] = eb[j + 1];
+    }
+    --k;
+  }
+  int64_t head = common_head(ptrs, eb, k, n);
   // TMA path: a 16-byte-alignable range of at least one tile whose pipeline
-  // shape fits in shared memory (all grad dtypes).
+  // shape fits in shared memory (all grad dtypes).  The fused reduce-scatter
+  // always uses the default shape (1024 threads x 3 stages, one CTA per SM).
+  const int64_t tile = gs.n > 0 ? 4 * 1024 : 4 * tma_cfg().nt;
   if ((gt == DOS_F32 || gt == DOS_F16 || gt == DOS_BF16) && (lt == DOS_NONE || lt == DOS_F16 || lt == DOS_BF16) &&
-      head >= 0 && tma_enabled() && tma_fits(gt, lt) && (n - head) / (4 * tma_cfg().nt) >= 1) {
-    const int64_t tile = 4 * tma_cfg().nt;
+      head >= 0 && tma_enabled() && (gs.n > 0 || tma_fits(gt, lt)) && (n - head) / tile >= 1) {
     const int64_t ntiles = (n - head) / tile;
     const int64_t tail = n - head - ntiles * tile;  // < one tile; handled inside the same launch
     const char* gc = static_cast<const char*>(g);
     char* lc = static_cast<char*>(lp);
     int rc = DOS_OK;
-    if (head > 0) rc = dos_adam_launch(p, m, v, g, gt, lp, lt, head, s, st, pr);  // < 8 elements: register path
+    if (head > 0) rc = dos_adam_launch(p, m, v, g, gt, lp, lt, head, s, st, pr, gs);  // < 8 elements: register path
     if (rc != DOS_OK) return rc;
     const void* gb = gc + (gt == DOS_F32 ? 4 : 2) * head;
     uint16_t* wb = lt == DOS_NONE ? nullptr : reinterpret_cast<uint16_t*>(lc + 2 * head);
     const dos_peers pb = dos_peers_offset(pr, head);
+    if (gs.n > 0) {
+      // fused reduce-scatter: the default pipeline shape only (see k_adam_tma)
+      const dos_gsrc gsb = dos_gsrc_offset(gs, head);
+      const int cpb = 1;
+      if (gt == DOS_BF16 && lt == DOS_BF16)
+        rc = launch_tma_cfg<DOS_BF16, DOS_BF16, 1024, 3, true>(p + head, m + head, v + head, gb, wb, ntiles, tail, s,
+                                                              cpb, st, pb, gsb);
+      else if (gt == DOS_F16 && lt == DOS_F16)
+        rc = launch_tma_cfg<DOS_F16, DOS_F16, 1024, 3, true>(p + head, m + head, v + head, gb, wb, ntiles, tail, s,
+                                                            cpb, st, pb, gsb);
+      else if (gt == DOS_BF16 && lt == DOS_NONE)
+        rc = launch_tma_cfg<DOS_BF16, DOS_NONE, 1024, 3, true>(p + head, m + head, v + head, gb, wb, ntiles, tail, s,
+                                                              cpb, st, pb, gsb);
+      else if (gt == DOS_F16 && lt == DOS_NONE)
+        rc = launch_tma_cfg<DOS_F16, DOS_NONE, 1024, 3, true>(p + head, m + head, v + head, gb, wb, ntiles, tail, s,
+                                                             cpb, st, pb, gsb);
+      else
+        return dos_set_error(DOS_ETYPE, "fused reduce-scatter: working copy must match the grad dtype (g=%d lowp=%d)",
+                             gt, lt);
+      if (rc != DOS_OK) return rc;
+      const cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return dos_set_error(DOS_ECUDA, "K1 (TMA, RS) launch failed: %s", cudaGetErrorString(e));
+      return DOS_OK;
+    }
 #define DOS_TMA(G, L) \
   if (gt == G && lt == L) rc = launch_adam_tma<G, L>(p + head, m + head, v + head, gb, wb, ntiles, tail, s, st, pb);
     DOS_TMA(DOS_F16, DOS_NONE) else DOS_TMA(DOS_F16, DOS_F16) else DOS_TMA(DOS_F16, DOS_BF16)
@@ -591,7 +754,7 @@ int dos_adam_launch(float* p, float* m, float* v, const void* g, int gt, void* l
     nvec = (n - head) / kVec;
   }
 #define DOS_CASE(G, L) \
-  if (gt == G && lt == L) { launch_adam<G, L>(p, m, v, g, lp, head, nvec, n, s, st, pr); }
+  if (gt == G && lt == L) { launch_adam<G, L>(p, m, v, g, lp, head, nvec, n, s, st, pr, gs); }
   DOS_CASE(DOS_F32, DOS_NONE) else DOS_CASE(DOS_F32, DOS_F16) else DOS_CASE(DOS_F32, DOS_BF16)
   else DOS_CASE(DOS_F16, DOS_NONE) else DOS_CASE(DOS_F16, DOS_F16) else DOS_CASE(DOS_F16, DOS_BF16)
   else DOS_CASE(DOS_BF16, DOS_NONE) else DOS_CASE(DOS_BF16, DOS_F16) else DOS_CASE(DOS_BF16, DOS_BF16)
@@ -681,3 +844,78 @@ extern "C" int dos_upscale_cuda(const void* x, int in_dtype, float* out, int64_t
 }
 
 extern "C" int64_t dos_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int dos_reduce_launch(void* out, int dt, int64_t n, const dos_gsrc& gs, cudaStream_t st) {
+  if (n == 0) return DOS_OK;
+  if (dt != DOS_F16 && dt != DOS_BF16) return dos_set_error(DOS_ETYPE, "reduce-scatter dtype %d unsupported", dt);
+  if (gs.n < 1 || gs.n > DOS_MAX_PEERS + 1) return dos_set_error(DOS_EINVAL, "reduce-scatter needs 1..%d sources", DOS_MAX_PEERS + 1);
+  const void* ptrs[DOS_MAX_PEERS + 2] = {out};
+  int eb[DOS_MAX_PEERS + 2] = {2};
+  for (int r = 0; r < gs.n; ++r) {
+    ptrs[1 + r] = gs.p[r];
+    eb[1 + r] = 2;
+  }
+  int64_t head = common_head(ptrs, eb, 1 + gs.n, n), nvec = 0;
+  if (head < 0) head = n; else nvec = (n - head) / kVec;
+  const unsigned grid = grid_for(nvec > 0 ? nvec : n);
+  uint16_t* o = static_cast<uint16_t*>(out);
+  if (dt == DOS_F16) k_reduce<DOS_F16><<<grid, kThreads, 0, st>>>(o, head, nvec, n, gs);
+  else k_reduce<DOS_BF16><<<grid, kThreads, 0, st>>>(o, head, nvec, n, gs);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return dos_set_error(DOS_ECUDA, "reduce-scatter launch failed: %s", cudaGetErrorString(e));
+  return DOS_OK;
+}
+
+namespace {
+int make_gsrc(const void* const* src, int nsrc, int self, float scale, dos_gsrc* out) {
+  if (nsrc < 1 || nsrc > DOS_MAX_PEERS + 1 || !src)
+    return dos_set_error(DOS_EINVAL, "nsrc must be in [1, %d] with source pointers", DOS_MAX_PEERS + 1);
+  if (self < 0 || self >= nsrc) return dos_set_error(DOS_EINVAL, "self rank %d outside [0, %d)", self, nsrc);
+  if (!(scale > 0.0f) || scale != scale) return dos_set_error(DOS_EINVAL, "grad scale must be positive");
+  out->n = nsrc;
+  out->self = self;
+  out->scale = scale;
+  for (int r = 0; r < nsrc; ++r) {
+    if (!src[r]) return dos_set_error(DOS_EINVAL, "NULL grad source %d", r);
+    out->p[r] = static_cast<const uint16_t*>(src[r]);
+  }
+  return DOS_OK;
+}
+}  // namespace
+
+extern "C" int dos_reduce_scatter_cuda(void* out, const void* const* src, int nsrc, int dtype, float scale,
+                                       int64_t n, void* stream) {
+  if (n < 0) return dos_set_error(DOS_EINVAL, "n must be >= 0");
+  if (dtype != DOS_F16 && dtype != DOS_BF16) return dos_set_error(DOS_ETYPE, "reduce-scatter dtype %d unsupported", dtype);
+  if (n > 0 && !out) return dos_set_error(DOS_EINVAL, "NULL output");
+  dos_gsrc gs;
+  const int rc = make_gsrc(src, nsrc, 0, scale, &gs);
+  if (rc != DOS_OK) return rc;
+  return dos_reduce_launch(out, dtype, n, gs, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int dos_adam_step_cuda_rs(float* p, float* m, float* v, const void* const* g_src, int nsrc, int self,
+                                     int g_dtype, float grad_scale, void* p_lowp, int lowp_dtype,
+                                     void* const* peer_lowp, int npeers, int64_t n, const dos_adam_scalars* s,
+                                     void* stream) {
+  if (!s) return dos_set_error(DOS_EINVAL, "scalars must not be NULL");
+  if (n < 0) return dos_set_error(DOS_EINVAL, "n must be >= 0");
+  if (g_dtype != DOS_F16 && g_dtype != DOS_BF16)
+    return dos_set_error(DOS_ETYPE, "the fused reduce-scatter takes 16-bit grads (dtype %d)", g_dtype);
+  if (lowp_dtype != DOS_NONE && lowp_dtype != g_dtype)
+    return dos_set_error(DOS_ETYPE, "working copy dtype %d must match the grads (%d)", lowp_dtype, g_dtype);
+  if (npeers < 0 || npeers > DOS_MAX_PEERS) return dos_set_error(DOS_EINVAL, "npeers must be in [0, %d]", DOS_MAX_PEERS);
+  if (npeers > 0 && (lowp_dtype == DOS_NONE || !peer_lowp)) return dos_set_error(DOS_EINVAL, "peers need a working copy");
+  if (n > 0 && (!p || !m || !v || (lowp_dtype != DOS_NONE && !p_lowp))) return dos_set_error(DOS_EINVAL, "NULL buffer");
+  dos_gsrc gs;
+  int rc = make_gsrc(g_src, nsrc, self, grad_scale, &gs);
+  if (rc != DOS_OK) return rc;
+  dos_peers pr{npeers, {}};
+  for (int r = 0; r < npeers; ++r) {
+    if (!peer_lowp[r]) return dos_set_error(DOS_EINVAL, "NULL peer pointer %d", r);
+    pr.p[r] = static_cast<uint16_t*>(peer_lowp[r]);
+  }
+  return dos_adam_launch(p, m, v, gs.p[self], g_dtype, p_lowp, lowp_dtype, n, dos_make_kscal(s),
+                         reinterpret_cast<cudaStream_t>(stream), pr, gs);
+}

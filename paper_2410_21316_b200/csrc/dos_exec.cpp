@@ -82,6 +82,7 @@ struct Engine {
   std::vector<int64_t> sg_start, sg_size, static_off;
   dos_kscal K{};
   dos_peers peers{0, {}};  // fused all-gather targets (shard element 0 in each peer)
+  dos_gsrc gsrc{0, 0, 1.0f, {}};  // fused reduce-scatter sources (shard element 0 in each rank)
   int32_t max_actions = 0, count = 0;
   std::vector<cudaEvent_t> ev_s, ev_e;
   cudaEvent_t ev0 = nullptr;
@@ -254,6 +255,11 @@ struct Engine {
         // §8(f) row 1 inside the phase: this subgroup's half-precision grads
         // D2H on their own stream, in emission (= subgroup) order
         const int64_t start = sg_start[sg], n = sg_size[sg];
+        if (gsrc.n > 0) {  // fused reduce-scatter of this subgroup, in place in dev_g, then the flush
+          const int rc = dos_reduce_launch(static_cast<char*>(const_cast<void*>(S.dev_g)) + 2 * start, S.lowp_dtype, n,
+                                           dos_gsrc_offset(gsrc, start), gst);
+          if (rc != DOS_OK) return fail(rc, dos_last_error());
+        }
         DOS_CU(cudaMemcpyAsync(static_cast<char*>(const_cast<void*>(S.host_g)) + 2 * start,
                                static_cast<const char*>(S.dev_g) + 2 * start, (size_t)n * 2, cudaMemcpyDeviceToHost,
                                gst));
@@ -338,14 +344,14 @@ struct Engine {
           // host_io: its grads were shipped H2D at phase start on the side stream
           if (S.host_io) DOS_CU(cudaStreamWaitEvent(s, ev_sg[sg], 0));
           return dos_adam_launch(S.dev_static_p + o, S.dev_static_m + o, S.dev_static_v + o, g, lt, lp, lt, n, K, s,
-                                 dos_peers_offset(peers, start));
+                                 dos_peers_offset(peers, start), dos_gsrc_offset(gsrc, start));
         }
         if (sg_slot[sg] < 0 || sg_mask[sg] != 7u)
           return dos_set_error(DOS_ESTATE, "fast update of subgroup %d with missing pieces (mask %u)", sg,
                                (unsigned)sg_mask[sg]);
         const int sl = sg_slot[sg];
         return dos_adam_launch(slot_ptr(sl, PIECE_P), slot_ptr(sl, PIECE_M), slot_ptr(sl, PIECE_V), g, lt, lp, lt, n,
-                               K, s, dos_peers_offset(peers, start));
+                               K, s, dos_peers_offset(peers, start), dos_gsrc_offset(gsrc, start));
       }
       case DOS_FLUSH_OUT_MODEL16:
         // K1 already stored the working copy in the same pass.
@@ -405,6 +411,23 @@ struct Engine {
       return dos_set_error(DOS_EINVAL, "npeers must be in [0, %d] with peer pointers", DOS_MAX_PEERS);
     peers.n = S.npeers;
     for (int r = 0; r < S.npeers; ++r) peers.p[r] = static_cast<uint16_t*>(S.peer_lowp[r]);
+    gsrc = dos_gsrc{0, 0, 1.0f, {}};
+    if (S.nsrc_g != 0) {
+      if (S.nsrc_g < 1 || S.nsrc_g > DOS_MAX_PEERS + 1 || !S.src_g)
+        return dos_set_error(DOS_EINVAL, "nsrc_g must be in [1, %d] with source pointers", DOS_MAX_PEERS + 1);
+      if (S.self_rank < 0 || S.self_rank >= S.nsrc_g || S.src_g[S.self_rank] != S.dev_g)
+        return dos_set_error(DOS_EINVAL, "src_g[self_rank] must be this rank's dev_g");
+      if (!S.flush_grads || S.host_io)
+        return dos_set_error(DOS_EINVAL, "the fused reduce-scatter needs flush_grads and excludes host_io");
+      if (!(S.grad_scale > 0.0f)) return dos_set_error(DOS_EINVAL, "grad_scale must be positive");
+      gsrc.n = S.nsrc_g;
+      gsrc.self = S.self_rank;
+      gsrc.scale = S.grad_scale;
+      for (int r = 0; r < S.nsrc_g; ++r) {
+        if (!S.src_g[r]) return dos_set_error(DOS_EINVAL, "NULL grad source %d", r);
+        gsrc.p[r] = static_cast<const uint16_t*>(S.src_g[r]);
+      }
+    }
     const int32_t cap = nmax > 0 ? nmax : 1;
     while ((int32_t)ev_s.size() < cap) {
       cudaEvent_t a, b, c;

@@ -25,9 +25,26 @@ struct dos_peers {
 };
 dos_peers dos_peers_offset(const dos_peers& pr, int64_t elems);
 
-// K1 launch without argument validation (used by the engine).
+// Sources of the fused reduce-scatter: p[r] is where the launch's range
+// starts in rank r's full-model grad buffer (16-bit, r = 0..n-1 in rank
+// order; p[self] is the local buffer).  The grad a kernel uses is
+// lowp(((w0 + w1) + w2) + ...) with fp32 RN adds in rank order, then
+// lowp(widen(that) * scale) if scale != 1 (ZeRO-3 averaging).  n == 0: off.
+struct dos_gsrc {
+  int n;
+  int self;
+  float scale;
+  const uint16_t* p[DOS_MAX_PEERS + 1];
+};
+dos_gsrc dos_gsrc_offset(const dos_gsrc& gs, int64_t elems);
+
+// K1 launch without argument validation (used by the engine).  With
+// gs.n > 0 the grads are the reduce-scatter of gs (g must be gs.p[gs.self]).
 int dos_adam_launch(float* p, float* m, float* v, const void* g, int gt, void* lp, int lt, int64_t n,
-                    const dos_kscal& s, cudaStream_t st, const dos_peers& pr = dos_peers{0, {}});
+                    const dos_kscal& s, cudaStream_t st, const dos_peers& pr = dos_peers{0, {}},
+                    const dos_gsrc& gs = dos_gsrc{0, 0, 1.0f, {}});
+// Stand-alone reduce-scatter of a range: out = the reduced grads of gs (n elements).
+int dos_reduce_launch(void* out, int dt, int64_t n, const dos_gsrc& gs, cudaStream_t st);
 
 // Host kernels (dos_host.cpp); the calling thread joins the team.
 int dos_host_adam(float* p, float* m, float* v, const void* g, int gt, void* lp, int lt, int64_t n,

@@ -185,15 +185,21 @@ class DeviceResidency:
             self._engines[key] = eng
         return eng
 
-    def state_desc(self, host_io: bool = False, peers=None, flush_grads: bool = False) -> tuple[N.dos_state_desc, list]:
+    def state_desc(self, host_io: bool = False, peers=None, flush_grads: bool = False,
+                   grad_sources=None) -> tuple[N.dos_state_desc, list]:
         """``peers``: addresses (ints) where this shard starts in each peer's
-        full-model buffer — the fused all-gather targets (include/dos.h)."""
+        full-model buffer — the fused all-gather targets (include/dos.h).
+        ``grad_sources``: a ``distributed.GradSources`` (fused reduce-scatter)."""
         opt = self.opt
         peers = list(peers or ())
         if len(peers) > N.DOS_MAX_PEERS:
             raise ValueError(f"at most {N.DOS_MAX_PEERS} peers")
         peer_arr = (C.c_void_p * max(1, len(peers)))(*peers)
-        keep = [self.sg_start, self.sg_size, self.static_off, peer_arr]
+        srcs = list(grad_sources.ptrs) if grad_sources is not None else []
+        if len(srcs) > N.DOS_MAX_PEERS + 1:
+            raise ValueError(f"at most {N.DOS_MAX_PEERS + 1} grad sources")
+        src_arr = (C.c_void_p * max(1, len(srcs)))(*srcs)
+        keep = [self.sg_start, self.sg_size, self.static_off, peer_arr, src_arr]
         p64 = C.POINTER(C.c_int64)
         d = N.dos_state_desc(
             num_subgroups=len(opt.subgroups),
@@ -211,6 +217,10 @@ class DeviceResidency:
             npeers=len(peers),
             peer_lowp=C.cast(peer_arr, C.POINTER(C.c_void_p)),
             flush_grads=1 if flush_grads else 0,
+            nsrc_g=len(srcs),
+            self_rank=grad_sources.self_rank if grad_sources is not None else 0,
+            src_g=C.cast(src_arr, C.POINTER(C.c_void_p)),
+            grad_scale=grad_sources.scale if grad_sources is not None else 1.0,
         )
         return d, keep
 
@@ -302,9 +312,11 @@ class B200Target(SimTarget):
 
     def __init__(self, profile: SystemProfile, plan: UpdatePlan, optimizer: ShardedOptimizer, hyper,
                  step: int, *, host_threads: int = 0, fuse_downscale: bool = True,
-                 host_io: bool = False, peers=None, flush_grads: bool = False) -> None:
+                 host_io: bool = False, peers=None, flush_grads: bool = False, grad_sources=None) -> None:
         if host_io and flush_grads:
             raise ValueError("host_io reads the grads from the host image; flush_grads copies them there")
+        if grad_sources is not None and not flush_grads:
+            raise ValueError("the fused reduce-scatter (grad_sources) runs with flush_grads=True")
         sizes = tuple(g.size for g in optimizer.subgroups)
         super().__init__(profile, plan, sizes)
         self.opt = optimizer
@@ -318,11 +330,12 @@ class B200Target(SimTarget):
         self.host_io = host_io
         self.peers = list(peers or ())
         self.flush_grads = flush_grads
+        self.grad_sources = grad_sources
         self._begun = False
         self._submitted = 0
 
     def _begin(self) -> None:
-        desc, keep = self.residency.state_desc(self.host_io, self.peers, self.flush_grads)
+        desc, keep = self.residency.state_desc(self.host_io, self.peers, self.flush_grads, self.grad_sources)
         self._keep = (desc, keep)
         h = self.hyper
         bc1, bc2 = bias_corrections(h.beta1, h.beta2, self.step)

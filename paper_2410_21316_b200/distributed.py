@@ -5,9 +5,10 @@ its fp32 optimizer state, its grads and its slice of the working copy.  The
 update phase itself is rank-local — no collective on the
 data path.  Around it:
 
-* before: **reduce-scatter** of the bf16 grads, bucketed per subgroup index
-  j (bucket j = every rank's subgroup j; each rank receives its own), so the
-  phase can start on bucket 0 while later buckets are still reducing;
+* before: **reduce-scatter** of the bf16 grads — fused into the phase
+  (``PeerGrads``: K1 sums every rank's grads of the shard over NVLink as it
+  streams the state), or bucketed NCCL per subgroup index j (bucket j =
+  every rank's subgroup j; each rank receives its own);
 * after: **all-gather** of the bf16 working copy, bucketed the same way.
   ``gather_params_overlapped`` makes a comm stream wait on the *engine event*
   of the action that finalises subgroup j's working copy (its GPU_UPDATE, or
@@ -150,6 +151,75 @@ class BucketedCollectives:
                 w.wait()
 
 
+def _ipc_bases(buf, group=None) -> dict[int, int]:
+    """Exchange CUDA IPC handles of ``buf`` (a device tensor) with every rank
+    of ``group`` and map theirs: rank -> base address of that rank's ``buf``
+    in this process (this rank maps to its own pointer)."""
+    import ctypes as C
+
+    import torch.distributed as dist
+
+    from . import _native as N
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    handle = C.create_string_buffer(64)
+    off = C.c_uint64()
+    N.check(N.lib().dos_ipc_export(buf.data_ptr(), handle, C.byref(off)))
+    everyone = [None] * world
+    dist.all_gather_object(everyone, (rank, handle.raw, off.value), group=group)
+    bases = {rank: buf.data_ptr()}
+    for r, h, o in everyone:
+        if r == rank:
+            continue
+        ptr = C.c_void_p()
+        N.check(N.lib().dos_ipc_import(h, o, C.byref(ptr)))
+        bases[r] = ptr.value
+    return bases
+
+
+@dataclass(frozen=True)
+class GradSources:
+    """The fused reduce-scatter's inputs for one rank (include/dos.h
+    ``dos_state_desc.src_g``): ``ptrs[r]`` is where this rank's shard starts
+    in rank r's full-model grad buffer, in rank order (``ptrs[self_rank]`` is
+    the local one); ``scale`` is applied after the sum (1/N to average)."""
+
+    ptrs: tuple[int, ...]
+    self_rank: int
+    scale: float = 1.0
+
+
+class PeerGrads:
+    """Every rank's full-model grad buffer mapped into this process (CUDA IPC,
+    one node): the sources of the reduce-scatter fused into the update phase.
+
+    Replaces the bucketed NCCL reduce-scatter before the phase: K1 reads the
+    shard's grads of every rank over NVLink and sums them in rank order while
+    it streams the fp32 state, and each host subgroup's grads are reduced on
+    the device right before their D2H flush.  The caller synchronises the
+    ranks before the phase (every backward done) and after it (no rank
+    overwrites grads a peer is still reading).
+    """
+
+    def __init__(self, full_grads, layout: ShardLayout, group=None) -> None:
+        import torch.distributed as dist
+
+        from . import _native as N
+
+        if full_grads.element_size() != 2:
+            raise TypeError("the full-model grad buffer must be half precision")
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        if self.world > N.DOS_MAX_PEERS + 1:
+            raise ValueError(f"fused reduce-scatter supports up to {N.DOS_MAX_PEERS + 1} ranks")
+        bases = _ipc_bases(full_grads, group)
+        shard_bytes = 2 * self.rank * layout.per_rank
+        self.ptrs = tuple(bases[r] + shard_bytes for r in range(self.world))
+        self.group = group
+
+    def sources(self, scale: float = 1.0) -> GradSources:
+        return GradSources(self.ptrs, self.rank, float(scale))
+
+
 class PeerTargets:
     """The fused all-gather's destinations: every peer's full-model buffer,
     mapped into this process with CUDA IPC (one node, NVLink/NVSwitch P2P).
@@ -164,8 +234,6 @@ class PeerTargets:
     """
 
     def __init__(self, full_params, layout: ShardLayout, group=None) -> None:
-        import ctypes as C
-
         import torch.distributed as dist
 
         from . import _native as N
@@ -175,19 +243,7 @@ class PeerTargets:
         rank, world = dist.get_rank(group), dist.get_world_size(group)
         if world - 1 > N.DOS_MAX_PEERS:
             raise ValueError(f"fused all-gather supports up to {N.DOS_MAX_PEERS + 1} ranks")
-        handle = C.create_string_buffer(64)
-        off = C.c_uint64()
-        N.check(N.lib().dos_ipc_export(full_params.data_ptr(), handle, C.byref(off)))
-        mine = (rank, handle.raw, off.value)
-        everyone = [None] * world
-        dist.all_gather_object(everyone, mine, group=group)
-        self.bases: dict[int, int] = {}
-        for r, h, o in everyone:
-            if r == rank:
-                continue
-            ptr = C.c_void_p()
-            N.check(N.lib().dos_ipc_import(h, o, C.byref(ptr)))
-            self.bases[r] = ptr.value
+        self.bases = {r: b for r, b in _ipc_bases(full_params, group).items() if r != rank}
         shard_bytes = 2 * rank * layout.per_rank
         self.targets = [self.bases[r] + shard_bytes for r in sorted(self.bases)]
         self.group = group

@@ -175,6 +175,7 @@ def execute_plan(
     peers=None,
     flush_grads: bool = False,
     fuse_downscale: bool = True,
+    grad_sources=None,
 ) -> ExecutionResult:
     """Run one optimizer step of ``plan`` on the B200; mutates ``optimizer``.
 
@@ -194,8 +195,13 @@ def execute_plan(
     the phase: the device grads of each host-updated subgroup are copied D2H
     on their own stream in subgroup order and each CPU_UPDATE waits only for
     its own subgroup (the upcast stays fused in H1).  ``peers`` enables the
-    fused all-gather (``distributed.PeerTargets``); ``on_submitted(target)``
-    runs after the last submit, before the wait.
+    fused all-gather (``distributed.PeerTargets``); ``grad_sources`` (a
+    ``distributed.GradSources``, with ``flush_grads=True``) the fused
+    reduce-scatter: this step's grads are the rank-order sum of every rank's
+    grads for this shard, reduced inside K1 (fast subgroups) or right before
+    the flush (host subgroups) and left in the device grads like a
+    reduce-scatter would.  ``on_submitted(target)`` runs after the last
+    submit, before the wait.
     """
     if plan.num_subgroups != len(optimizer.subgroups):
         raise ValueError(f"plan covers {plan.num_subgroups} subgroups, optimizer has {len(optimizer.subgroups)}")
@@ -203,7 +209,8 @@ def execute_plan(
         raise ValueError("throttle_scale must be positive")
     step = optimizer.step + 1
     target = B200Target(profile, plan, optimizer, hyper, step, host_threads=host_threads, host_io=host_io,
-                        peers=peers, flush_grads=flush_grads, fuse_downscale=fuse_downscale)
+                        peers=peers, flush_grads=flush_grads, fuse_downscale=fuse_downscale,
+                        grad_sources=grad_sources)
     try:
         events = run_update(plan, target)
         if on_submitted is not None:  # e.g. chain per-subgroup collectives onto engine events

@@ -13,8 +13,13 @@ ZeRO-3 sharded (``shard(P, N, SG)``, core.py:139-170): each rank keeps the
 fp32 master params, Adam m and v of its own chunk in its pinned host pool,
 and ``step()`` runs
 
-1. a bucketed reduce-scatter of the bf16 grads into this rank's chunk
-   (summed; ``average_grads`` divides by N),
+1. the reduce-scatter of the bf16 grads into this rank's chunk (summed;
+   ``average_grads`` divides by N) — by default fused into the phase: K1
+   reads every rank's grads of the shard over NVLink (CUDA IPC,
+   ``distributed.PeerGrads``) and sums them in rank order while it streams
+   the fp32 state, and each host subgroup's grads are reduced on the device
+   right before their D2H flush; with ``fused_reduce=False`` a bucketed NCCL
+   reduce-scatter runs before the phase,
 2. inside the phase, the D2H flush of the grads the host lane will read
    (§8(f) row 1; ``execute_plan(flush_grads=True)``),
 3. the update phase (``execute_plan``) with the all-gather fused in: K1
@@ -33,7 +38,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import policy
-from .distributed import BucketedCollectives, PeerTargets, ShardLayout, gather_params_overlapped
+from .distributed import BucketedCollectives, PeerGrads, PeerTargets, ShardLayout, gather_params_overlapped
 from .executor import AdamHyper, execute_plan
 from .plan import Device, build_plan
 from .state import ShardedOptimizer, lowp_downscale
@@ -43,7 +48,7 @@ class DeepOptimizerStates:
     def __init__(self, params, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 0.0,
                  *, subgroup_size: int = 100_000_000, profile=None, stride="auto", static_ratio: float = 0.0,
                  master_params=None, process_group=None, average_grads: bool = False, explore: int = 3,
-                 fused_gather: bool = True) -> None:
+                 fused_gather: bool = True, fused_reduce: bool = True) -> None:
         import torch
         import torch.distributed as dist
 
@@ -99,6 +104,8 @@ class DeepOptimizerStates:
         # fused all-gather: K1 writes the working copy straight into every
         # peer's full-model buffer (IPC-mapped); else bucketed overlapped gathers
         self.peers = PeerTargets(self.flat, lay, process_group) if (self.world > 1 and fused_gather) else None
+        # fused reduce-scatter: every rank's grad buffer IPC-mapped, reduced inside the phase
+        self.peer_grads = PeerGrads(self.flat_grad, lay, process_group) if (self.world > 1 and fused_reduce) else None
 
         if profile is None:
             from .catalog import get_profile
@@ -143,6 +150,11 @@ class DeepOptimizerStates:
                 host[sg.start:sg.stop].copy_(g[sg.start:sg.stop], non_blocking=True)
         torch.cuda.current_stream(self.res.device).synchronize()
 
+    def _barrier(self) -> None:
+        import torch.distributed as dist
+
+        dist.barrier(group=self.group)
+
     def _max_over_ranks(self, x: float) -> float:
         if self.world == 1:
             return x
@@ -159,7 +171,11 @@ class DeepOptimizerStates:
         import torch
 
         torch.cuda.current_stream(self.res.device).synchronize()  # backward done
-        if self.coll is not None:
+        gsrc = None
+        if self.peer_grads is not None:
+            self._barrier()  # every rank's grads are complete before any rank reads them
+            gsrc = self.peer_grads.sources(1.0 / self.world if self.average_grads else 1.0)
+        elif self.coll is not None:
             self._reduce_grads()
             torch.cuda.current_stream(self.res.device).synchronize()
         hook = None
@@ -167,14 +183,17 @@ class DeepOptimizerStates:
             hook = gather_params_overlapped(self.coll, self.plan, self.res.model16, self.flat)
         # the host lane's grads are flushed D2H inside the phase (flush_grads)
         self.last = execute_plan(self.opt, self.plan, self.profile, self.hyper, on_submitted=hook,
-                                 peers=self.peers.targets if self.peers is not None else None, flush_grads=True)
+                                 peers=self.peers.targets if self.peers is not None else None, flush_grads=True,
+                                 grad_sources=gsrc)
         if hook is not None:
             for w in hook.works:
                 if w is not None:
                     w.wait()
             torch.cuda.current_stream(self.res.device).wait_stream(hook.stream)
-        if self.peers is not None:
-            self.peers.barrier()  # every rank's peer stores have landed (each finished its phase)
+        if self.peers is not None or self.peer_grads is not None:
+            # every rank's peer stores have landed and no rank still reads a
+            # peer's grads (each finished its phase) before anyone moves on
+            self._barrier()
         if self.tuner is not None and self.last.measured is not None:
             self.tuner.record(self.plan.stride, int(self._max_over_ranks(self.last.measured.span_ns)))
             nxt = self.tuner.next_stride()

@@ -83,3 +83,27 @@ def test_acceptance_instances_digests():
         st = O.initialize(inst["total"], inst["sg"], inst["seed"])
         O.sequential_oracle(st, **inst["hyper"])
         assert O.state_digest(st) == inst["digest"], inst
+
+
+@pytest.mark.parametrize("lowp", ["bf16", "fp16"])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+@pytest.mark.parametrize("scale", [1.0, 0.5, 1.0 / 3])
+def test_reduce_scatter_oracle_matches_torch_loop(lowp, world, scale):
+    """oracle.reduce_scatter (declared semantics; the reference has no
+    collectives) against an independent torch CPU statement of the same
+    rule: rank-order fp32 adds, one cast, scale, cast."""
+    torch = pytest.importorskip("torch")
+    tdt = torch.bfloat16 if lowp == "bf16" else torch.float16
+    rng = np.random.default_rng(world)
+    xs = [torch.from_numpy(rng.normal(0, 1.0, 50_000).astype(np.float32)).to(tdt) for _ in range(world)]
+    acc = xs[0].float()
+    for x in xs[1:]:
+        acc = acc + x.float()
+    want = acc.to(tdt)
+    if scale != 1.0:
+        want = (want.float() * torch.tensor(scale, dtype=torch.float32)).to(tdt)
+    srcs = [x.view(torch.int16).numpy().view(np.uint16) for x in xs]
+    if lowp == "fp16":
+        srcs = [s.view(np.float16) for s in srcs]
+    got = O.reduce_scatter(srcs, lowp, scale)
+    assert np.asarray(got).view(np.uint16).tobytes() == want.view(torch.int16).numpy().view(np.uint16).tobytes()
