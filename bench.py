@@ -470,8 +470,8 @@ class B200Bench:
         if self.world == 1:
             return
         torch, D = self.torch, self.D
-        from paper_2410_21316_b200.distributed import (BucketedCollectives, PeerTargets, ShardLayout,
-                                                       gather_params_overlapped)
+        from paper_2410_21316_b200.distributed import (BucketedCollectives, GradSources, PeerGrads, PeerTargets,
+                                                       ShardLayout, gather_params_overlapped)
 
         lay = ShardLayout.build(self.P, self.world, self.SG)
         coll = BucketedCollectives(lay)
@@ -491,27 +491,46 @@ class B200Bench:
                     w.wait()
 
         phase_ag = self.timed(overlapped, 1)
-        peers, why = None, ""
+        peers, pgrads, why = None, None, ""
+        fullg = torch.zeros(lay.padded_total, dtype=tdt, device=self.device)  # every rank's full-model grads
         try:
             peers = PeerTargets(full, lay)
+            pgrads = PeerGrads(fullg, lay)
         except Exception as exc:  # e.g. no P2P between these GPUs
             why = str(exc)[:160]
         # every rank must agree before anyone waits in the fused phase's barrier
-        if -self.max_over_ranks(-1.0 if peers is not None else 0.0) >= 1.0:
+        if -self.max_over_ranks(-1.0 if pgrads is not None else 0.0) >= 1.0:
             def fused():
                 D.execute_plan(self.opt, self.plan, self.profile, self.hyper, peers=peers.targets)
                 peers.barrier()
 
             fused_ms = self.timed(fused, 1)
+            # the reduce-scatter fused too: the peers' grads of this shard are read
+            # over NVLink by K1 / the host subgroups' reduce (this rank's own grads
+            # are the residency's); flush inside the phase; barriers on both sides
+            ptrs = list(pgrads.ptrs)
+            ptrs[self.rank] = self.opt.residency.grads.data_ptr()
+            gsrc = GradSources(tuple(ptrs), self.rank, 1.0)
+
+            def fused_all():
+                self.barrier()
+                D.execute_plan(self.opt, self.plan, self.profile, self.hyper, peers=peers.targets, flush_grads=True,
+                               grad_sources=gsrc)
+                self.barrier()
+
+            fused_all_ms = self.timed(fused_all, 1)
         else:
-            fused_ms = f"unavailable: {why or 'a peer could not map the IPC buffers'}"
+            fused_ms = fused_all_ms = f"unavailable: {why or 'a peer could not map the IPC buffers'}"
         best = min(phase_ag, fused_ms) if isinstance(fused_ms, float) else phase_ag
+        nccl_iter = rs_ms + best
         self.out["collectives"] = {
             "reduce_scatter_ms": rs_ms, "all_gather_ms": ag_ms, "buckets": lay.num_buckets,
             "bytes_per_rank_each": 2 * lay.padded_total,
             "phase_with_overlapped_all_gather_ms": phase_ag, "phase_with_fused_all_gather_ms": fused_ms,
-            "iteration_update_ms": rs_ms + best}
-        self.out["iteration"]["iteration_update_ms"] += rs_ms
+            "phase_with_fused_reduce_scatter_and_all_gather_ms": fused_all_ms,
+            "iteration_update_ms": min(nccl_iter, fused_all_ms) if isinstance(fused_all_ms, float) else nccl_iter}
+        self.out["iteration"]["iteration_update_ms"] = min(self.out["iteration"]["iteration_update_ms"] + rs_ms,
+                                                           self.out["collectives"]["iteration_update_ms"])
 
     def static_variants(self) -> None:
         """the same phase with a fraction of the subgroups'
