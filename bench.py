@@ -453,15 +453,34 @@ class B200Bench:
             self.out["e2e"] = None
             return
         D, opt, plan = self.D, self.opt, self.plan
-        fast = sum(s for i, s in enumerate(self.sizes) if plan.devices[i] is D.Device.FAST)
         D.execute_plan(opt, plan, self.profile, self.hyper, host_io=True)  # warm the mode
-        ms = self.timed(lambda: D.execute_plan(opt, plan, self.profile, self.hyper, host_io=True), self.args.steps)
+        tried = None
+        if self.args.stride == "auto" and plan.stride is not D.ALL_CPU:
+            # host buffers shift the link/host balance (grads H2D and the working
+            # copy D2H for fast subgroups, no grad flush for host ones): re-tune
+            # the stride for this mode, hill-climbing from the device-mode choice
+            tuner = self.policy.StrideTuner(self.profile, self.sizes, range(1, 7), self.args.static_ratio, explore=1)
+            tuner.queue = [plan.stride]
+            while tuner.exploring:
+                k = tuner.next_stride()
+                tuner.record(k, self.timed(lambda: D.execute_plan(opt, tuner.plan_for(k), self.profile, self.hyper,
+                                                                  host_io=True), 1))
+            plan = tuner.plan()
+            tried = {str(k): v for k, v in sorted(tuner.measured.items())}
+        fast = sum(s for i, s in enumerate(self.sizes) if plan.devices[i] is D.Device.FAST)
+        last = []
+        ms = self.timed(lambda: last.append(D.execute_plan(opt, plan, self.profile, self.hyper, host_io=True)),
+                        self.args.steps)
+        ev = last[-1].timeline.events  # the plan's link bytes (SimTarget.bytes_of), + host_io's 2+2 B per fast param
+        h2d_b = sum(e.bytes for e in ev if e.action.lane.value == "h2d")
+        d2h_b = sum(e.bytes for e in ev if e.action.lane.value == "d2h")
         self.out["e2e"] = {
             "value": self.P / (ms * 1e-3), "unit": UNIT,
-            "h2d_bytes_per_step": (2 * fast + self.h2d_b) * self.world,
-            "d2h_bytes_per_step": (2 * fast + self.d2h_b) * self.world, "ms_per_step": ms,
+            "h2d_bytes_per_step": (2 * fast + h2d_b) * self.world,
+            "d2h_bytes_per_step": (2 * fast + d2h_b) * self.world, "ms_per_step": ms,
             "api": "execute_plan(..., host_io=True): grads from pinned host, working copy back to host",
-            "host_resident_params": (self.P_rank - fast) * self.world}
+            "host_resident_params": (self.P_rank - fast) * self.world, "stride": plan.stride,
+            "measured_ms_by_stride": tried}
 
     def collectives(self) -> None:
         """N > 1: bucketed NCCL reduce-scatter of the grads, the all-gather of

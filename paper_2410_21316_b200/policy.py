@@ -150,11 +150,19 @@ class StrideTuner:
     used.  This captures what the closed-form and simulated models do not —
     on a host whose DRAM is shared by the H1 threads and the copy engines,
     host traffic slows the DMA (measured on the B200 box: 50 -> 29-35 GB/s).
+
+    With ``hill_climb`` the exploration does not stop at the predicted
+    candidates: while the fastest measured stride has an unmeasured
+    neighbour (stride ± 1, within 1..number of subgroups), that neighbour is
+    tried next, so the tuner ends on a measured local minimum even when the
+    model's ranking is off by more than the explored set.  Decisions depend
+    only on the recorded spans, so ranks that record the same (max-over-
+    ranks) spans stay in lockstep.
     """
 
     def __init__(self, profile: SystemProfile, sizes: Sequence[int], candidates: Iterable = range(1, 7),
                  static_ratio: float = 0.0, explore: int = 4, num_slots: int = 2,
-                 link_slowdown: float = 1.0) -> None:
+                 link_slowdown: float = 1.0, hill_climb: bool = True) -> None:
         self.sizes = list(sizes)
         self.static_ratio = static_ratio
         best, spans = choose_stride(profile, self.sizes, candidates, static_ratio, num_slots, link_slowdown)
@@ -162,6 +170,7 @@ class StrideTuner:
         self.queue = ranked[:max(1, explore)]
         self.predicted = spans
         self.measured: dict = {}
+        self.hill_climb = hill_climb
 
     def next_stride(self):
         if self.queue:
@@ -172,6 +181,11 @@ class StrideTuner:
         self.measured[stride] = min(span_ns, self.measured.get(stride, span_ns))
         if self.queue and self.queue[0] == stride:
             self.queue.pop(0)
+        if self.hill_climb and not self.queue:
+            best = min(self.measured, key=lambda k: self.measured[k])
+            if best is not ALL_CPU:
+                top = max(1, len(self.sizes))
+                self.queue = [k for k in (best + 1, best - 1) if 1 <= k <= top and k not in self.measured][:1]
 
     @property
     def exploring(self) -> bool:

@@ -321,7 +321,7 @@ def test_b200_model_timelines_validate_without_stream_fifo(h100):
 def test_stride_tuner_explores_then_exploits(h100):
     from paper_2410_21316_b200 import policy
 
-    tuner = policy.StrideTuner(h100, [10**8] * 20, range(1, 7), explore=3)
+    tuner = policy.StrideTuner(h100, [10**8] * 20, range(1, 7), explore=3, hill_climb=False)
     tried = []
     fake = {1: 900, 2: 500, 3: 400, 4: 450, 5: 700, 6: 800}
     while tuner.exploring:
@@ -331,6 +331,27 @@ def test_stride_tuner_explores_then_exploits(h100):
     assert len(tried) == 3 and len(set(tried)) == 3
     assert tuner.next_stride() == min(tried, key=fake.get)
     assert tuner.plan().stride == tuner.next_stride()
+
+
+@pytest.mark.parametrize("optimum", [1, 3, 6, 9, 14, 20])
+def test_stride_tuner_hill_climbs_past_the_predicted_set(h100, optimum):
+    """The measured optimum may lie outside the model's top candidates (on the
+    B200 box the best stride sits at the edge of the predicted range): the
+    tuner walks to a measured local minimum and stops there."""
+    from paper_2410_21316_b200 import policy
+
+    n = 20
+    tuner = policy.StrideTuner(h100, [10**8] * n, range(1, 7), explore=3)
+    fake = lambda k: 1000 + 37 * abs(k - optimum)  # unimodal in the stride
+    tried = []
+    while tuner.exploring:
+        k = tuner.next_stride()
+        assert 1 <= k <= n and k not in tried
+        tried.append(k)
+        tuner.record(k, fake(k))
+        assert len(tried) <= n
+    assert tuner.next_stride() == optimum
+    assert all(k in tuner.measured for k in (optimum - 1, optimum + 1) if 1 <= k <= n)
 
 
 def test_refit_profile_from_a_timeline(h100):
