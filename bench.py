@@ -55,8 +55,8 @@ def parse():
                          "the paper's representative setting (PAPER.md:631-635); the rest is host-offloaded")
     ap.add_argument("--capacity-gb", type=float, default=None,
                     help="imposed dynamic fast-tier budget (default: two windows)")
-    ap.add_argument("--cpu-sample", type=int, default=25,
-                    help="1e8-param subgroups timed for the cpu_baseline (~10 s on 16 cores)")
+    ap.add_argument("--cpu-sample", type=int, default=70,
+                    help="1e8-param subgroups timed for the cpu_baseline (70 = one full 7B phase, ~25 core-seconds)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--host-threads", type=int, default=0, help="H1 team size (0: all allowed cores / ranks)")
     ap.add_argument("--trace-dir", default=None, help="write measured/predicted timelines as trace CSVs")
@@ -64,6 +64,8 @@ def parse():
                     help="process-group backend for N>1 (gloo: dry run with ranks sharing GPUs)")
     ap.add_argument("--no-ref-schedule", action="store_true",
                     help="skip timing the reference's ALL_CPU offload schedule on this runtime")
+    ap.add_argument("--no-copy-streams", action="store_true",
+                    help="skip the pure-streaming (link-bound) copy-stream measurement")
     ap.add_argument("--static-variants", default="0.0,0.5,1.0",
                     help="extra measured runs with HBM-resident static subgroups ('' to skip)")
     return ap.parse_args()
@@ -567,6 +569,55 @@ class B200Bench:
                              "hbm_resident_state_bytes": 12 * sum(self.sizes[i] for i in vplan.static_set) * self.world})
         self.out["static_variants"] = variants
 
+    def copy_streams(self) -> None:
+        """north_star: the copy streams at >= 80% of the measured host link
+        with the update fully overlapped.  Measured on the pure-streaming plan
+        (stride 1, no residents: every subgroup's fp32 p/m/v crosses the link
+        both ways, 12 B/param per direction, no host-lane work), where the link
+        is the bound; its denominator is the duplex pinned copy measured here
+        (1 GiB each way at once, best of 3)."""
+        if self.args.no_copy_streams:
+            self.out["copy_streams"] = None
+            return
+        D = self.D
+        link = self.profile_b200.measure_link(1 << 30)
+        splan = D.build_plan(self.nsg, 1, static_ratio=0.0)
+        D.execute_plan(self.opt, splan, self.profile, self.hyper)  # moves any residents home
+        res: list = []
+        ms = self.timed(lambda: res.append(D.execute_plan(self.opt, splan, self.profile, self.hyper)),
+                        self.args.steps)
+        ev = res[-1].timeline.events
+        h2d_b = sum(e.bytes for e in ev if e.action.lane.value == "h2d")
+        d2h_b = sum(e.bytes for e in ev if e.action.lane.value == "d2h")
+
+        def union_ns(r, lanes) -> int:
+            iv = sorted((e.start_ns, e.end_ns) for e in r.measured.events if e.action.lane.value in lanes)
+            tot, cur_s, cur_e = 0, None, None
+            for s, e in iv:
+                if cur_e is None or s > cur_e:
+                    tot += 0 if cur_e is None else cur_e - cur_s
+                    cur_s, cur_e = s, e
+                else:
+                    cur_e = max(cur_e, e)
+            return tot + (0 if cur_e is None else cur_e - cur_s)
+
+        spans = [r.measured.span_ns for r in res]
+        link_ns = [union_ns(r, ("h2d", "d2h")) for r in res]
+        k1_ns = [sum(e.duration_ns for e in r.measured.events if e.action.lane.value == "fast_compute") for r in res]
+        duplex = link["duplex_GBs_per_dir"]
+        per_dir = {"h2d": h2d_b / (ms * 1e-3) / 1e9, "d2h": d2h_b / (ms * 1e-3) / 1e9}
+        self.out["copy_streams"] = {
+            "plan": "stride 1, static_ratio 0 (every subgroup streamed through the B200)",
+            "ms_per_step": ms, "value": self.P / (ms * 1e-3),
+            "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
+            "achieved_GBs_per_dir": per_dir, "link_measured_GBs": link,
+            "frac": min(per_dir.values()) / duplex, "peak": duplex, "peak_source": "duplex pinned copy, measured here",
+            # K1 runs while the link is busy: the time the link sits idle inside
+            # the span is the update's exposed part (pipeline fill + drain included)
+            "update_busy_ms": float(np.median(k1_ns)) / 1e6,
+            "link_idle_in_span_ms": float(np.median([s - l for s, l in zip(spans, link_ns)])) / 1e6,
+            "subgroups_streamed": self.nsg}
+
     def reference_schedule(self) -> None:
         """The reference's offload-to-CPU schedule (ALL_CPU blocking plan,
         scheduler.py:301-319) executed by this runtime on the same box."""
@@ -629,6 +680,7 @@ class B200Bench:
         self.e2e()
         self.collectives()
         self.static_variants()
+        self.copy_streams()
         self.reference_schedule()
         self.traces()
         if self.rank == 0:
