@@ -50,9 +50,10 @@ def parse():
     ap.add_argument("--subgroup", type=float, default=1e8)
     ap.add_argument("--lowp", default="bf16", choices=["bf16", "fp16"])
     ap.add_argument("--stride", default="auto")
-    ap.add_argument("--static-ratio", type=float, default=0.2,
+    ap.add_argument("--static-ratio", default="0.2",
                     help="fraction of subgroups whose fp32 state stays in HBM (TwinFlow-style residents); 0.2 is "
-                         "the paper's representative setting (PAPER.md:631-635); the rest is host-offloaded")
+                         "the paper's representative setting (PAPER.md:631-635); the rest is host-offloaded. 'auto': as many "
+                         "as fit in HBM (capacity-aware)")
     ap.add_argument("--capacity-gb", type=float, default=None,
                     help="imposed dynamic fast-tier budget (default: two windows)")
     ap.add_argument("--cpu-sample", type=int, default=70,
@@ -127,11 +128,15 @@ class ClockSampler:
 
 
 def fill_shard(opt, seed: int, device) -> None:
-    """Seeded synthetic state generated on the device, subgroup by subgroup,
-    copied into the pinned host pool (numpy init of 7B would take ~10 min).
-    Distributions of core.py:259-272: p~N(0,.02), m~N(0,1e-3), v~U*1e-4, g~N(0,1)."""
+    """Seeded synthetic state generated on the device, subgroup by subgroup
+    (numpy init of 7B would take ~10 min), written to each subgroup's home:
+    the HBM allocation of a static resident, else the pinned host pool; the
+    grads and working copy go to HBM and, for host-homed subgroups, to their
+    host images too.  Distributions of core.py:259-272: p~N(0,.02),
+    m~N(0,1e-3), v~U*1e-4, g~N(0,1)."""
     import torch
 
+    res = opt.residency
     gen = torch.Generator(device=device)
     to_t = lambda a: torch.from_numpy(a.view(np.int16) if a.itemsize == 2 else a)
     tdt = torch.bfloat16 if opt.lowp == "bf16" else torch.float16
@@ -142,12 +147,29 @@ def fill_shard(opt, seed: int, device) -> None:
         m = torch.randn(n, generator=gen, device=device) * 1e-3
         v = torch.rand(n, generator=gen, device=device) * 1e-4
         g = torch.randn(n, generator=gen, device=device).to(tdt)
+        w = p.to(tdt)
+        res.grads[sl].copy_(g)
+        res.model16[sl].copy_(w)
+        if sg.index in res.static_set:
+            for dst, src in zip(res.static_views(sg.index), (p, m, v)):
+                dst.copy_(src)
+            continue
         to_t(opt._p[sl]).copy_(p)
         to_t(opt._m[sl]).copy_(m)
         to_t(opt._v[sl]).copy_(v)
         to_t(opt._g[sl]).copy_(g.view(torch.int16))
-        to_t(opt._w[sl]).copy_(p.to(tdt).view(torch.int16))
+        to_t(opt._w[sl]).copy_(w.view(torch.int16))
     torch.cuda.synchronize()
+
+
+def host_available_bytes() -> int:
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 1 << 62
 
 
 def cpu_oracle_rate(sg: int, nsub: int, lowp: str, threads: int) -> dict:
@@ -288,17 +310,30 @@ class B200Bench:
                       f"oracle/adam_oracle.c (reference loop restated) with {threads} threads"}
 
     def setup(self) -> None:
-        D = self.D
+        D, a, torch = self.D, self.args, self.torch
         mine = D.shard(self.P, self.world, self.SG)[self.rank]
         self.P_rank = sum(g.size for g in mine)
-        t0 = time.perf_counter()
-        self.opt = D.ShardedOptimizer.allocate(self.P_rank, self.SG, lowp=self.args.lowp)
-        t1 = time.perf_counter()
-        fill_shard(self.opt, seed=1234 + self.rank, device=self.device)
-        self.opt.to_device(self.device)
-        self.out["setup_s"] = {"alloc_pin": t1 - t0, "fill": time.perf_counter() - t1}
-        self.sizes = [g.size for g in self.opt.subgroups]
+        self.sizes = [g.size for g in mine]
         self.nsg = len(self.sizes)
+        if a.static_ratio == "auto":
+            # capacity-aware residency: as many subgroups homed in HBM as fit
+            # beside the grads, the working copy and two windows
+            free = torch.cuda.mem_get_info(self.device)[0]
+            ratio = self.policy.capacity_static_ratio(self.sizes, free)
+            self.static_ratio = -self.max_over_ranks(-ratio)  # same plan shape on every rank
+        else:
+            self.static_ratio = float(a.static_ratio)
+        static = D.build_plan(self.nsg, 1, static_ratio=self.static_ratio).static_set
+        t0 = time.perf_counter()
+        # sparse pinned pool: host memory only for the host-homed subgroups
+        self.opt = D.ShardedOptimizer.allocate(self.P_rank, self.SG, lowp=a.lowp,
+                                               host_homed=[i for i in range(self.nsg) if i not in static])
+        t1 = time.perf_counter()
+        res = self.opt.to_device(self.device)
+        res.set_static(static)
+        fill_shard(self.opt, seed=1234 + self.rank, device=self.device)
+        self.out["setup_s"] = {"alloc_pin": t1 - t0, "fill": time.perf_counter() - t1}
+        self.out["host_pinned_bytes"] = self.opt.host_bytes
         cap = None if self.args.capacity_gb is None else int(self.args.capacity_gb * 1e9)
         self.cap = cap
         self.profile = self.profile_b200.measure_profile(fast_capacity_bytes=cap, quick=True)
@@ -316,15 +351,23 @@ class B200Bench:
             stride = D.ALL_CPU
         else:
             stride = int(a.stride)
-        self.plan = D.build_plan(self.nsg, stride, static_ratio=a.static_ratio)
+        self.plan = D.build_plan(self.nsg, stride, static_ratio=self.static_ratio)
         if a.stride == "auto":
             r = D.execute_plan(self.opt, self.plan, self.profile, self.hyper)
             self.profile = self.broadcast(self.policy.refit_profile(self.profile, r.measured, self.sizes))
-            tuner = self.tune(a.static_ratio, explore=4)
+            tuner = self.tune(self.static_ratio, explore=4)
             self.stride_spans = tuner.predicted
             self.plan = tuner.plan()
             self.tuned = {str(k): v / 1e6 for k, v in sorted(tuner.measured.items())}
         self.stride = self.plan.stride
+
+    def host_fits(self, ratio: float) -> bool:
+        """Would homing every non-static subgroup on the host (16 B/param
+        pinned) fit in the host memory still available?"""
+        static = self.D.build_plan(self.nsg, 1, static_ratio=ratio).static_set
+        need = 16 * sum(s for i, s in enumerate(self.sizes) if i not in static)
+        ok = need <= self.opt.host_bytes + host_available_bytes() - (8 << 30)
+        return -self.max_over_ranks(-1.0 if ok else 0.0) >= 1.0
 
     def tune(self, ratio: float, explore: int):
         D = self.D
@@ -461,7 +504,7 @@ class B200Bench:
             # host buffers shift the link/host balance (grads H2D and the working
             # copy D2H for fast subgroups, no grad flush for host ones): re-tune
             # the stride for this mode, hill-climbing from the device-mode choice
-            tuner = self.policy.StrideTuner(self.profile, self.sizes, range(1, 7), self.args.static_ratio, explore=1)
+            tuner = self.policy.StrideTuner(self.profile, self.sizes, range(1, 7), self.static_ratio, explore=1)
             tuner.queue = [plan.stride]
             while tuner.exploring:
                 k = tuner.next_stride()
@@ -560,6 +603,9 @@ class B200Bench:
         variants = []
         for tok in [t for t in self.args.static_variants.split(",") if t.strip()]:
             ratio = float(tok)
+            if not self.host_fits(ratio):
+                variants.append({"static_ratio": ratio, "skipped": "host-homed state would not fit in host memory"})
+                continue
             tuner = self.tune(ratio, explore=3)  # untimed; the first step also moves the residents
             vplan = tuner.plan()
             D.execute_plan(self.opt, vplan, self.profile, self.hyper)
@@ -580,6 +626,9 @@ class B200Bench:
             self.out["copy_streams"] = None
             return
         D = self.D
+        if not self.host_fits(0.0):
+            self.out["copy_streams"] = {"skipped": "the whole shard would not fit in pinned host memory"}
+            return
         link = self.profile_b200.measure_link(1 << 30)
         splan = D.build_plan(self.nsg, 1, static_ratio=0.0)
         D.execute_plan(self.opt, splan, self.profile, self.hyper)  # moves any residents home
@@ -625,6 +674,9 @@ class B200Bench:
             self.out["reference_offload_schedule"] = None
             return
         D = self.D
+        if not self.host_fits(0.0):
+            self.out["reference_offload_schedule"] = {"skipped": "the whole shard would not fit in pinned host memory"}
+            return
         rplan = D.build_plan(self.nsg, D.ALL_CPU)
         D.execute_plan(self.opt, rplan, self.profile, self.hyper)
         ms = self.timed(lambda: D.execute_plan(self.opt, rplan, self.profile, self.hyper), 2)
@@ -646,16 +698,20 @@ class B200Bench:
     def line(self) -> dict:
         D, a, prof = self.D, self.args, self.profile
         windows = 2 if self.cap is None else min(2, self.cap // (12 * self.SG))
+        which = {125_000_000: " (BASELINE configs[0])", 7_000_000_000: " (BASELINE configs[1])",
+                 13_000_000_000: " (BASELINE configs[2])"}.get(self.P, "")
+        r = self.static_ratio
         config = {
             "workload": f"{self.P / 1e9:g}B-param fp32 Adam shard, {a.lowp} grads + working copy, "
-                        f"host offload of {100 * (1 - a.static_ratio):g}% of the optimizer state "
-                        f"({100 * a.static_ratio:g}% HBM-resident, TwinFlow-style) (BASELINE configs[1])",
+                        f"host offload of {100 * (1 - r):.4g}% of the optimizer state "
+                        f"({100 * r:.4g}% HBM-resident, TwinFlow-style"
+                        f"{', capacity-aware' if a.static_ratio == 'auto' else ''}){which}",
             "params": self.P, "subgroup": self.SG, "subgroups_per_rank": self.nsg, "lowp": a.lowp,
             "stride": "all_cpu" if self.stride is D.ALL_CPU else self.stride,
             "planner_k": "all_cpu" if self.choice.k is D.ALL_CPU else self.choice.k, "k_real": self.choice.k_real,
             "predicted_span_ms_by_stride": None if self.stride_spans is None else
             {str(k): v / 1e6 for k, v in self.stride_spans.items()},
-            "measured_span_ms_by_stride": self.tuned, "static_ratio": a.static_ratio,
+            "measured_span_ms_by_stride": self.tuned, "static_ratio": r,
             "fast_capacity_bytes": self.cap, "hbm_windows": windows,
             "parallelism": f"zero3-shard{self.world}", "l2": "inputs > L2 (28 B/param over 1e8-param subgroups)"}
         line = {"metric": METRIC, "value": self.P / (self.ms * 1e-3), "unit": UNIT, "n_gpus": self.world,

@@ -124,6 +124,16 @@ int dos_upscale_cuda(const void* x, int in_dtype, float* out, int64_t n, void* s
  * and register_cuda != 0).  numa_node < 0: no binding. */
 int dos_host_alloc(size_t bytes, int numa_node, int register_cuda, void** out);
 int dos_host_free(void* ptr);
+/* Sparse pool regions: reserve address space for a whole flat array, commit
+ * (first touch + page-lock + register) only the byte ranges homed on the
+ * host.  Committed runs that touch are merged into one registration.
+ * dos_host_committed returns the committed bytes (or a negative DOS_E*).
+ * dos_host_free releases either kind.  Replaces core.py:208-272's dense
+ * allocation of every array for the whole shard: subgroups whose fp32 state
+ * is homed in HBM cost no host memory. */
+int dos_host_reserve(size_t bytes, int numa_node, int register_cuda, void** out);
+int dos_host_commit(void* base, size_t offset, size_t len);
+int64_t dos_host_committed(void* base);
 int dos_host_threads(void); /* size of the library's host team */
 int dos_set_host_threads(int n);
 
@@ -202,6 +212,12 @@ typedef struct dos_state_desc {
   int32_t self_rank;
   const void* const* src_g;
   float grad_scale;
+  /* Optional per-subgroup HBM homes of the static residents' fp32 state:
+   * dev_static_sg[3*i + {0,1,2}] = p, m, v of subgroup i (NULL when not
+   * static).  When non-NULL it replaces dev_static_{p,m,v} + static_offset[i]
+   * (static_offset[i] >= 0 still marks residency), so the static set can
+   * grow and shrink one subgroup at a time without re-packing HBM. */
+  float* const* dev_static_sg;
 } dos_state_desc;
 
 #define DOS_MAX_PEERS 7

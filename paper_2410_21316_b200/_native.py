@@ -62,6 +62,7 @@ class dos_state_desc(C.Structure):
         ("self_rank", C.c_int32),
         ("src_g", C.POINTER(C.c_void_p)),
         ("grad_scale", C.c_float),
+        ("dev_static_sg", C.POINTER(C.c_void_p)),
     ]
 
 
@@ -105,6 +106,9 @@ SIGNATURES: dict[str, tuple] = {
     "dos_upscale_cuda": (_I, [_VP, _I, _VP, _I64, _VP]),
     "dos_host_alloc": (_I, [_SZ, _I, _I, C.POINTER(_VP)]),
     "dos_host_free": (_I, [_VP]),
+    "dos_host_reserve": (_I, [_SZ, _I, _I, C.POINTER(_VP)]),
+    "dos_host_commit": (_I, [_VP, _SZ, _SZ]),
+    "dos_host_committed": (C.c_int64, [_VP]),
     "dos_host_threads": (_I, []),
     "dos_set_host_threads": (_I, [_I]),
     "dos_exec_create": (_I, [C.POINTER(dos_exec_config), C.POINTER(_VP)]),
@@ -189,13 +193,30 @@ def scalars(lr: float, beta1: float, beta2: float, eps: float, bc1, bc2,
 
 
 class HostBuffer:
-    """A region of the pinned host pool (dos_host_alloc), freed on GC."""
+    """A region of the pinned host pool, freed on GC.
 
-    def __init__(self, nbytes: int, numa_node: int = -1, register_cuda: bool = True):
+    Dense (default, dos_host_alloc): committed and registered whole.
+    ``sparse=True`` (dos_host_reserve): address space only; ``commit`` makes
+    byte ranges resident, page-locked and registered (dos_host_commit)."""
+
+    def __init__(self, nbytes: int, numa_node: int = -1, register_cuda: bool = True, sparse: bool = False):
         out = C.c_void_p()
-        check(lib().dos_host_alloc(int(nbytes), int(numa_node), 1 if register_cuda else 0, C.byref(out)))
+        fn = lib().dos_host_reserve if sparse else lib().dos_host_alloc
+        check(fn(int(nbytes), int(numa_node), 1 if register_cuda else 0, C.byref(out)))
         self.address = out.value
         self.nbytes = int(nbytes)
+        self.sparse = sparse
+
+    def commit(self, offset_bytes: int, nbytes: int) -> None:
+        if offset_bytes < 0 or nbytes < 0 or offset_bytes + nbytes > self.nbytes:
+            raise ValueError("commit range exceeds the host buffer")
+        check(lib().dos_host_commit(self.address, int(offset_bytes), int(nbytes)))
+
+    @property
+    def committed_bytes(self) -> int:
+        n = lib().dos_host_committed(self.address)
+        check(int(n) if n < 0 else 0)
+        return int(n)
 
     def array(self, dtype, count: int, offset_bytes: int = 0) -> np.ndarray:
         dt = np.dtype(dtype)

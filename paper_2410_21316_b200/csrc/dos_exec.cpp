@@ -343,8 +343,12 @@ struct Engine {
           if (o < 0) return dos_set_error(DOS_ESTATE, "subgroup %d marked static but has no HBM residence", sg);
           // host_io: its grads were shipped H2D at phase start on the side stream
           if (S.host_io) DOS_CU(cudaStreamWaitEvent(s, ev_sg[sg], 0));
-          return dos_adam_launch(S.dev_static_p + o, S.dev_static_m + o, S.dev_static_v + o, g, lt, lp, lt, n, K, s,
-                                 dos_peers_offset(peers, start), dos_gsrc_offset(gsrc, start));
+          float* sp = S.dev_static_sg ? S.dev_static_sg[3 * sg] : S.dev_static_p + o;
+          float* sm = S.dev_static_sg ? S.dev_static_sg[3 * sg + 1] : S.dev_static_m + o;
+          float* sv = S.dev_static_sg ? S.dev_static_sg[3 * sg + 2] : S.dev_static_v + o;
+          if (!sp || !sm || !sv) return dos_set_error(DOS_ESTATE, "static subgroup %d has no HBM state", sg);
+          return dos_adam_launch(sp, sm, sv, g, lt, lp, lt, n, K, s, dos_peers_offset(peers, start),
+                                 dos_gsrc_offset(gsrc, start));
         }
         if (sg_slot[sg] < 0 || sg_mask[sg] != 7u)
           return dos_set_error(DOS_ESTATE, "fast update of subgroup %d with missing pieces (mask %u)", sg,

@@ -24,6 +24,7 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <map>
 #include <unordered_map>
 #include <vector>
 
@@ -247,6 +248,9 @@ namespace {
 struct Region {
   size_t bytes;
   bool registered;
+  bool sparse;                      // dos_host_reserve: committed piecewise
+  std::map<size_t, size_t> runs;    // sparse: committed [first, last) 2 MB pages, one registration each
+  bool register_cuda;
 };
 std::mutex g_pool_mu;
 std::unordered_map<void*, Region> g_regions;
@@ -299,10 +303,104 @@ extern "C" int dos_host_alloc(size_t bytes, int numa_node, int register_cuda, vo
   }
   {
     std::lock_guard<std::mutex> lk(g_pool_mu);
-    g_regions[ptr] = Region{len, registered};
+    g_regions[ptr] = Region{len, registered, false, {}, false};
   }
   *out = ptr;
   return DOS_OK;
+}
+
+// Sparse regions: the address space of a whole flat array is reserved up
+// front, but memory is committed (touched, then page-locked and registered)
+// only for the ranges that are homed on the host — the subgroups whose fp32
+// state lives in HBM never cost host RAM.  Committed runs that touch are
+// merged into one registration, so a copy that stays inside a committed run
+// is always a pinned DMA.
+extern "C" int dos_host_reserve(size_t bytes, int numa_node, int register_cuda, void** out) {
+  if (!out) return dos_set_error(DOS_EINVAL, "out must not be NULL");
+  *out = nullptr;
+  if (bytes == 0) bytes = 1;
+  const size_t huge = size_t(2) << 20;
+  const size_t len = (bytes + huge - 1) & ~(huge - 1);
+  void* ptr = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
+  if (ptr == MAP_FAILED) return dos_set_error(DOS_ESYS, "mmap(%zu) failed: %s", len, strerror(errno));
+  madvise(ptr, len, MADV_HUGEPAGE);
+  if (numa_node >= 0 && numa_node < 64) {
+    unsigned long mask = 1ul << numa_node;
+    sys_mbind(ptr, len, 2 /* MPOL_BIND */, &mask, 64, 0);  // best effort, as dos_host_alloc
+  }
+  int ndev = 0;
+  const bool reg = register_cuda && cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0;
+  if (!reg) cudaGetLastError();
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_regions[ptr] = Region{len, false, true, {}, reg};
+  }
+  *out = ptr;
+  return DOS_OK;
+}
+
+extern "C" int dos_host_commit(void* base, size_t offset, size_t len) {
+  if (len == 0) return DOS_OK;
+  const size_t huge = size_t(2) << 20;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  auto it = g_regions.find(base);
+  if (it == g_regions.end()) return dos_set_error(DOS_EINVAL, "pointer %p was not allocated by the host pool", base);
+  Region& r = it->second;
+  if (!r.sparse) return DOS_OK;  // a dense region is committed whole
+  if (offset > r.bytes || len > r.bytes - offset)
+    return dos_set_error(DOS_EINVAL, "commit [%zu, +%zu) outside the %zu-byte region", offset, len, r.bytes);
+  size_t lo = offset / huge, hi = (offset + len + huge - 1) / huge;
+  // runs overlapping or adjacent to [lo, hi) merge into one
+  std::vector<std::pair<size_t, size_t>> merged;
+  for (auto& kv : r.runs) {
+    if (kv.first <= lo && kv.second >= hi) return DOS_OK;  // already committed
+    if (kv.second >= lo && kv.first <= hi) merged.push_back(kv);
+  }
+  size_t nlo = lo, nhi = hi;
+  for (auto& kv : merged) {
+    nlo = std::min(nlo, kv.first);
+    nhi = std::max(nhi, kv.second);
+  }
+  char* b = static_cast<char*>(base);
+  for (auto& kv : merged) {
+    if (r.register_cuda) cudaHostUnregister(b + kv.first * huge);
+    r.runs.erase(kv.first);
+  }
+  // first touch of the new pages in parallel (read + write back, so pages that
+  // were faulted in earlier keep their contents)
+  const int64_t npages4k = (int64_t)((nhi - nlo) * huge / 4096);
+  char* start = b + nlo * huge;
+  parallel_chunks(npages4k, 0, [&](int64_t a, int64_t e) {
+    for (int64_t i = a; i < e; ++i) {
+      volatile char* c = start + i * 4096;
+      *c = *c;
+    }
+  });
+  if (r.register_cuda) {
+    const cudaError_t e = cudaHostRegister(start, (nhi - nlo) * huge, cudaHostRegisterDefault);
+    if (e != cudaSuccess) {
+      // leave the previously committed runs registered as they were
+      for (auto& kv : merged)
+        if (cudaHostRegister(b + kv.first * huge, (kv.second - kv.first) * huge, cudaHostRegisterDefault) ==
+            cudaSuccess)
+          r.runs[kv.first] = kv.second;
+      return dos_set_error(DOS_ECUDA, "cudaHostRegister(%zu) failed: %s", (nhi - nlo) * huge,
+                           cudaGetErrorString(e));
+    }
+  }
+  r.runs[nlo] = nhi;
+  return DOS_OK;
+}
+
+extern "C" int64_t dos_host_committed(void* base) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  auto it = g_regions.find(base);
+  if (it == g_regions.end()) return dos_set_error(DOS_EINVAL, "pointer %p was not allocated by the host pool", base);
+  const Region& r = it->second;
+  if (!r.sparse) return (int64_t)r.bytes;
+  size_t pages = 0;
+  for (auto& kv : r.runs) pages += kv.second - kv.first;
+  return (int64_t)(pages * (size_t(2) << 20));
 }
 
 extern "C" int dos_host_free(void* ptr) {
@@ -316,6 +414,8 @@ extern "C" int dos_host_free(void* ptr) {
     g_regions.erase(it);
   }
   if (r.registered) cudaHostUnregister(ptr);
+  if (r.register_cuda)
+    for (auto& kv : r.runs) cudaHostUnregister(static_cast<char*>(ptr) + kv.first * (size_t(2) << 20));
   munmap(ptr, r.bytes);
   return DOS_OK;
 }

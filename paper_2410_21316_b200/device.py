@@ -6,11 +6,16 @@ Memory layout of one rank on the B200 (HBM) and its host (pinned pool):
   -------------------------          ---
   params32/momentum32/variance32     grads        lowp[P]   (resident: backward/RS writes it)
     fp32[P] — home tier of every     model16      lowp[P]   (authoritative working copy)
-    dynamic and CPU subgroup         static p/m/v fp32, compact, for static residents
+    dynamic and CPU subgroup         static p/m/v fp32, one allocation per static resident
   grads16   lowp[P] — host image     slots[num_slots] x {m, v, p} fp32[SG_max]
     used by CPU subgroups              (the in-flight windows; engine-owned)
   model16   lowp[P] — staging for
     CPU-downscaled params (H2D_PARAMS16 source) and the lazy host image
+
+A sparse host pool (``ShardedOptimizer.allocate(host_homed=...)``) commits
+host memory only for subgroups homed on the host; a static resident's home is
+then its HBM allocation alone, and its host range is committed only if it
+leaves the static set (or the caller reads the full host arrays).
 
 ``B200Target`` is the third implementation of the reference's UpdateTarget
 protocol (pkg/src/optistate/scheduler.py:388-399), after SimTarget and
@@ -70,8 +75,9 @@ class DeviceResidency:
         self.sg_start = np.array([g.start for g in opt.subgroups], dtype=np.int64)
         self.sg_size = np.array([g.size for g in opt.subgroups], dtype=np.int64)
         self.static_set: frozenset[int] = frozenset()
-        self.static_off = np.full(nsg, -1, dtype=np.int64)
-        self.static_p = self.static_m = self.static_v = None
+        self.static_off = np.full(nsg, -1, dtype=np.int64)  # >= 0: HBM-resident (engine marker)
+        self.static_sg: dict[int, tuple] = {}  # subgroup -> (p, m, v) fp32 HBM tensors
+        self._static_ptrs = (C.c_void_p * max(1, 3 * nsg))()
         self.host_stale: set[str] = set()  # host images behind the device
         self._engines: dict[tuple, "Engine"] = {}
         self.push_host()
@@ -87,11 +93,26 @@ class DeviceResidency:
         torch.from_numpy(dst.view(np.int16 if dst.itemsize == 2 else np.int32)).copy_(
             src.view(torch.int16 if src.element_size() == 2 else torch.int32), non_blocking=False)
 
+    def _h2d_lowp(self, dst, src: np.ndarray) -> None:
+        """Upload a half-precision host array; ranges not committed in a
+        sparse pool read as zeros, so they are zero-filled on the device."""
+        runs = self.opt.host_runs("lowp")
+        if runs == [(0, self.opt.total_params)]:
+            self._h2d(dst, src)
+            return
+        dst.zero_()
+        for a, b in runs:
+            self._h2d(dst[a:b], src[a:b])
+
+    def _d2h_lowp(self, dst: np.ndarray, src) -> None:
+        for a, b in self.opt.host_runs("lowp"):
+            self._d2h(dst[a:b], src[a:b])
+
     def push_host(self) -> None:
         """Host arrays became authoritative (init, a host-side update): re-upload."""
         opt = self.opt
-        self._h2d(self.grads, opt._g)
-        self._h2d(self.model16, opt._w)
+        self._h2d_lowp(self.grads, opt._g)
+        self._h2d_lowp(self.model16, opt._w)
         for sg in self.static_set:
             self._upload_static(sg)
         self.host_stale.clear()
@@ -102,13 +123,28 @@ class DeviceResidency:
         self.host_stale.discard(name)
         opt = self.opt
         if name == "_w":
-            self._d2h(opt._w, self.model16)
+            self._d2h_lowp(opt._w, self.model16)
             return
-        src = {"_p": self.static_p, "_m": self.static_m, "_v": self.static_v}[name]
+        k = ("_p", "_m", "_v").index(name)
         dst = getattr(opt, name)
+        opt.ensure_host(self.static_set, "state")
         for sg in self.static_set:
-            a, n, o = int(self.sg_start[sg]), int(self.sg_size[sg]), int(self.static_off[sg])
-            self._d2h(dst[a:a + n], src[o:o + n])
+            a, n = int(self.sg_start[sg]), int(self.sg_size[sg])
+            self._d2h(dst[a:a + n], self.static_sg[sg][k])
+
+    def on_host_commit(self, subgroups, group: str) -> None:
+        """A sparse pool just committed these subgroups' host ranges (they
+        read as zeros): copy in what the device holds for them — the grads
+        and working copy ("lowp"), or a static resident's fp32 state."""
+        opt = self.opt
+        for sg in subgroups:
+            a, n = int(self.sg_start[sg]), int(self.sg_size[sg])
+            if group == "lowp":
+                self._d2h(opt._g[a:a + n], self.grads[a:a + n])
+                self._d2h(opt._w[a:a + n], self.model16[a:a + n])
+            elif sg in self.static_sg:
+                for k, name in enumerate(("_p", "_m", "_v")):
+                    self._d2h(getattr(opt, name)[a:a + n], self.static_sg[sg][k])
 
     def sync_all_host(self) -> None:
         for name in ("_w", "_p", "_m", "_v"):
@@ -129,42 +165,65 @@ class DeviceResidency:
                 raise ValueError("grads must hold total_params elements")
             src = grads.reshape(-1).to(device=self.device, dtype=self.tdtype)
             self.grads.copy_(src)
-            self._d2h(opt._g, self.grads)
+            self._d2h_lowp(opt._g, self.grads)
             return
         arr = np.asarray(grads)
         if arr.dtype != opt._g.dtype or arr.shape != opt._g.shape:
             raise TypeError(f"grads must be {opt._g.dtype}{opt._g.shape}")
-        opt._g[:] = arr
+        opt.grads16[:] = arr  # (a full host write: commits every range of a sparse pool)
         self._h2d(self.grads, opt._g)
 
     def _upload_static(self, sg: int) -> None:
-        a, n, o = int(self.sg_start[sg]), int(self.sg_size[sg]), int(self.static_off[sg])
-        self._h2d(self.static_p[o:o + n], self.opt._p[a:a + n])
-        self._h2d(self.static_m[o:o + n], self.opt._m[a:a + n])
-        self._h2d(self.static_v[o:o + n], self.opt._v[a:a + n])
+        """Host image -> the subgroup's HBM home (zeros where a sparse pool
+        never committed the range: that is what the host image holds)."""
+        a, n = int(self.sg_start[sg]), int(self.sg_size[sg])
+        for k, name in enumerate(("_p", "_m", "_v")):
+            dst = self.static_sg[sg][k]
+            if self.opt.host_committed(sg, "state"):
+                self._h2d(dst, getattr(self.opt, name)[a:a + n])
+            else:
+                dst.zero_()
+
+    def static_views(self, sg: int) -> tuple:
+        """(p, m, v) fp32 HBM tensors of static subgroup ``sg`` (its home
+        while resident: write them to initialise a device-homed subgroup)."""
+        if sg not in self.static_sg:
+            raise ValueError(f"subgroup {sg} is not HBM-resident")
+        return self.static_sg[sg]
 
     def set_static(self, static_set: frozenset[int]) -> None:
-        """Make exactly ``static_set`` HBM-resident (TwinFlow-style statics)."""
+        """Make exactly ``static_set`` HBM-resident (TwinFlow-style statics).
+
+        Each resident owns its own HBM allocation, so the set changes one
+        subgroup at a time: leaving subgroups are written back to (and, in a
+        sparse pool, committed on) the host and freed before joining ones are
+        allocated and uploaded; staying ones do not move."""
+        static_set = frozenset(static_set)
         if static_set == self.static_set:
             return
         torch = _torch()
-        for name in ("_p", "_m", "_v"):
-            self.sync_host(name)
-        self.static_set = frozenset(static_set)
-        self.static_off[:] = -1
-        off = 0
-        for sg in sorted(self.static_set):
-            self.static_off[sg] = off
-            off += int(self.sg_size[sg])
-        if off:
-            with torch.cuda.device(self.device):
-                self.static_p = torch.empty(off, dtype=torch.float32, device=self.device)
-                self.static_m = torch.empty(off, dtype=torch.float32, device=self.device)
-                self.static_v = torch.empty(off, dtype=torch.float32, device=self.device)
-            for sg in self.static_set:
+        opt = self.opt
+        leaving = sorted(self.static_set - static_set)
+        joining = sorted(static_set - self.static_set)
+        if leaving:
+            opt.ensure_host(leaving, "state")
+            for sg in leaving:
+                a, n = int(self.sg_start[sg]), int(self.sg_size[sg])
+                for k, name in enumerate(("_p", "_m", "_v")):
+                    self._d2h(getattr(opt, name)[a:a + n], self.static_sg[sg][k])
+                del self.static_sg[sg]
+                self.static_off[sg] = -1
+                for k in range(3):
+                    self._static_ptrs[3 * sg + k] = None
+        with torch.cuda.device(self.device):
+            for sg in joining:
+                n = int(self.sg_size[sg])
+                self.static_sg[sg] = tuple(torch.empty(n, dtype=torch.float32, device=self.device) for _ in range(3))
                 self._upload_static(sg)
-        else:
-            self.static_p = self.static_m = self.static_v = None
+                self.static_off[sg] = 0
+                for k in range(3):
+                    self._static_ptrs[3 * sg + k] = self.static_sg[sg][k].data_ptr()
+        self.static_set = static_set
 
     def after_phase(self, host_io: bool = False) -> None:
         if not host_io:  # with host_io the engine mirrored the working copy to the host
@@ -199,7 +258,7 @@ class DeviceResidency:
         if len(srcs) > N.DOS_MAX_PEERS + 1:
             raise ValueError(f"at most {N.DOS_MAX_PEERS + 1} grad sources")
         src_arr = (C.c_void_p * max(1, len(srcs)))(*srcs)
-        keep = [self.sg_start, self.sg_size, self.static_off, peer_arr, src_arr]
+        keep = [self.sg_start, self.sg_size, self.static_off, peer_arr, src_arr, self._static_ptrs]
         p64 = C.POINTER(C.c_int64)
         d = N.dos_state_desc(
             num_subgroups=len(opt.subgroups),
@@ -210,9 +269,8 @@ class DeviceResidency:
             host_p=N.ptr(opt._p), host_m=N.ptr(opt._m), host_v=N.ptr(opt._v),
             host_g=N.ptr(opt._g), host_lowp=N.ptr(opt._w),
             dev_g=self.grads.data_ptr(), dev_lowp=self.model16.data_ptr(),
-            dev_static_p=self.static_p.data_ptr() if self.static_p is not None else None,
-            dev_static_m=self.static_m.data_ptr() if self.static_m is not None else None,
-            dev_static_v=self.static_v.data_ptr() if self.static_v is not None else None,
+            dev_static_p=None, dev_static_m=None, dev_static_v=None,
+            dev_static_sg=C.cast(self._static_ptrs, C.POINTER(C.c_void_p)),
             host_io=1 if host_io else 0,
             npeers=len(peers),
             peer_lowp=C.cast(peer_arr, C.POINTER(C.c_void_p)),
@@ -324,6 +382,12 @@ class B200Target(SimTarget):
         self.step = step
         self.residency = optimizer.to_device()
         self.residency.set_static(plan.static_set)
+        # a sparse pool commits what this plan reads or writes on the host
+        # (no-ops for a dense pool or ranges already committed)
+        nsg = len(sizes)
+        optimizer.ensure_host([i for i in range(nsg) if i not in plan.static_set], "state")
+        optimizer.ensure_host(range(nsg) if host_io else
+                              [i for i in range(nsg) if plan.devices[i].value == "cpu"], "lowp")
         self.num_slots, slot_elems = slots_for(profile, plan, sizes)
         self.engine = self.residency.engine(self.num_slots, slot_elems, host_threads, fuse_downscale)
         self._descs = plan_descs(plan)

@@ -201,3 +201,24 @@ class StrideTuner:
 def fast_fraction(plan: UpdatePlan, sizes: Sequence[int]) -> float:
     tot = sum(sizes)
     return sum(s for i, s in enumerate(sizes) if plan.devices[i] is Device.FAST) / tot if tot else 0.0
+
+
+def capacity_static_ratio(sizes: Sequence[int], free_hbm_bytes: int, *, lowp_bytes_per_param: int = 4,
+                          windows: int = 2, headroom_bytes: int = 4 << 30) -> float:
+    """SURVEY §8(f) row 2, capacity-aware: the largest TwinFlow static ratio
+    whose residents fit in the HBM left after the half-precision grads and
+    working copy (``lowp_bytes_per_param`` for the whole shard), ``windows``
+    in-flight subgroup windows and a headroom.  Residents are counted at the
+    largest subgroup size (placement may take the ragged tail or not), and the
+    returned ratio reproduces the count exactly through the reference rule
+    ``floor(ratio * N + 1e-9)`` (scheduler.py:161-168)."""
+    n = len(sizes)
+    if n == 0:
+        return 0.0
+    big = max(sizes)
+    budget = free_hbm_bytes - headroom_bytes - lowp_bytes_per_param * sum(sizes)
+    budget -= windows * 12 * big
+    count = max(0, min(n, budget // (12 * big)))
+    if count == n:  # nothing streams: no windows needed
+        count = n if free_hbm_bytes - headroom_bytes - (lowp_bytes_per_param + 12) * sum(sizes) >= 0 else n - 1
+    return count / n

@@ -299,9 +299,53 @@ class ShardedOptimizer:
         self._w, self._g = model16, grads16
         self._total = total
         self.residency: DeviceResidency | None = None
+        # sparse host pool (allocate(host_homed=...)): per array group, which
+        # subgroups' host ranges are committed; None = dense (all committed)
+        self._sparse: dict | None = None
+
+    # -- sparse host pool
+    _GROUPS = {"state": ("_p", "_m", "_v"), "lowp": ("_g", "_w")}
+
+    def host_committed(self, sg: int, group: str = "state") -> bool:
+        return self._sparse is None or bool(self._sparse[group][sg])
+
+    def ensure_host(self, subgroups, group: str = "state") -> None:
+        """Commit (touch, page-lock, register) the host ranges of ``subgroups``
+        in the arrays of ``group`` ("state": p/m/v, "lowp": grads/working copy).
+        No-op for a dense pool or ranges already committed."""
+        if self._sparse is None:
+            return
+        have = self._sparse[group]
+        todo = sorted(i for i in subgroups if not have[i])
+        if not todo:
+            return
+        for a, b in _runs([self.subgroups[i] for i in todo]):
+            for name in self._GROUPS[group]:
+                arr = getattr(self, name)
+                self._sparse["bufs"][name].commit(a * arr.itemsize, (b - a) * arr.itemsize)
+        have[todo] = True
+        if self.residency is not None:  # fill the new host ranges from the device where it is authoritative
+            self.residency.on_host_commit(todo, group)
+
+    def host_runs(self, group: str = "state") -> list[tuple[int, int]]:
+        """Element ranges ``[a, b)`` whose host images are committed (merged)."""
+        if self._sparse is None:
+            return [(0, self._total)] if self._total else []
+        have = self._sparse[group]
+        return _runs([g for g in self.subgroups if have[g.index]])
+
+    @property
+    def host_bytes(self) -> int:
+        """Host memory committed for this shard's arrays."""
+        arrays = (self._p, self._m, self._v, self._g, self._w)
+        if self._sparse is None:
+            return sum(a.nbytes for a in arrays)
+        return sum(self._sparse["bufs"][n].committed_bytes for n in ("_p", "_m", "_v", "_g", "_w"))
 
     # -- host views (lazily refreshed from the device when it is authoritative)
     def _host(self, name: str) -> np.ndarray:
+        if self._sparse is not None:  # a full-array read materialises every range
+            self.ensure_host(range(len(self.subgroups)), "state" if name in ("_p", "_m", "_v") else "lowp")
         if self.residency is not None:
             self.residency.sync_host(name)
         return getattr(self, name)
@@ -324,6 +368,8 @@ class ShardedOptimizer:
 
     @property
     def grads16(self) -> np.ndarray:
+        if self._sparse is not None:
+            self.ensure_host(range(len(self.subgroups)), "lowp")
         return self._g
 
     @property
@@ -337,19 +383,45 @@ class ShardedOptimizer:
     # -- construction
     @classmethod
     def allocate(cls, total_params: int, subgroup_size: int, lowp: str = "fp16",
-                 numa_node: int = -1) -> "ShardedOptimizer":
-        """Zero-filled state in the pinned pool (no RNG)."""
+                 numa_node: int = -1, host_homed=None) -> "ShardedOptimizer":
+        """Zero-filled state in the pinned pool (no RNG).
+
+        ``host_homed``: None commits every array for the whole shard (the
+        reference's layout, core.py:208-272).  A collection of subgroup
+        indices reserves the address space but commits host memory only for
+        those subgroups — the rest are to be homed in HBM as static residents
+        (``DeviceResidency.set_static``), so a shard whose state exceeds the
+        host RAM still runs.  Uncommitted ranges read as zeros and are
+        committed on demand (``ensure_host``, or any full-array read).
+        """
         groups = shard(total_params, 1, subgroup_size)[0]
         dt16 = _LOWP_NP[lowp]
-        return cls(
-            subgroups=groups,
-            params32=pinned_empty(total_params, np.float32, numa_node),
-            momentum32=pinned_empty(total_params, np.float32, numa_node),
-            variance32=pinned_empty(total_params, np.float32, numa_node),
-            model16=pinned_empty(total_params, dt16, numa_node),
-            grads16=pinned_empty(total_params, dt16, numa_node),
-            lowp=lowp,
-        )
+        if host_homed is None:
+            return cls(
+                subgroups=groups,
+                params32=pinned_empty(total_params, np.float32, numa_node),
+                momentum32=pinned_empty(total_params, np.float32, numa_node),
+                variance32=pinned_empty(total_params, np.float32, numa_node),
+                model16=pinned_empty(total_params, dt16, numa_node),
+                grads16=pinned_empty(total_params, dt16, numa_node),
+                lowp=lowp,
+            )
+        homed = sorted({int(i) for i in host_homed})
+        if homed and (homed[0] < 0 or homed[-1] >= len(groups)):
+            raise ValueError(f"host_homed indices must be in [0, {len(groups)})")
+        bufs, arrays = {}, {}
+        for name, dt in (("_p", np.float32), ("_m", np.float32), ("_v", np.float32), ("_w", dt16), ("_g", dt16)):
+            dt = np.dtype(dt)
+            hb = N.HostBuffer(max(1, dt.itemsize * total_params), numa_node=numa_node, sparse=True)
+            bufs[name] = hb
+            arrays[name] = hb.array(dt, total_params)
+        opt = cls(subgroups=groups, params32=arrays["_p"], momentum32=arrays["_m"], variance32=arrays["_v"],
+                  model16=arrays["_w"], grads16=arrays["_g"], lowp=lowp)
+        opt._sparse = {"bufs": bufs, "state": np.zeros(len(groups), dtype=bool),
+                       "lowp": np.zeros(len(groups), dtype=bool)}
+        opt.ensure_host(homed, "state")
+        opt.ensure_host(homed, "lowp")
+        return opt
 
     @classmethod
     def initialize(cls, total_params: int, subgroup_size: int, seed: int = 0,
@@ -414,6 +486,17 @@ class ShardedOptimizer:
         if arr.dtype != self._g.dtype or arr.shape != self._g.shape:
             raise TypeError(f"grads must be {self._g.dtype}{self._g.shape}")
         self._g[:] = arr
+
+
+def _runs(subgroups) -> list[tuple[int, int]]:
+    """Merged element ranges covered by ``subgroups``."""
+    out: list[list[int]] = []
+    for g in sorted(subgroups, key=lambda g: g.start):
+        if out and g.start <= out[-1][1]:
+            out[-1][1] = max(out[-1][1], g.stop)
+        else:
+            out.append([g.start, g.stop])
+    return [(a, b) for a, b in out]
 
 
 def bias_corrections(beta1: float, beta2: float, step: int) -> tuple[np.float32, np.float32]:

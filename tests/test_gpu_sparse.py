@@ -1,0 +1,95 @@
+"""Sparse host pool + per-subgroup HBM homes on the B200: a shard whose
+static residents never touch host memory runs the update phase bit-exactly
+against the oracle, the phase commits no host memory, and the static set can
+shrink and grow between steps (subgroups move home one at a time)."""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import optistate_oracle as O
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+import paper_2410_21316_b200 as D  # noqa: E402
+from paper_2410_21316_b200 import Placement  # noqa: E402
+
+HYPER = D.AdamHyper()
+
+
+def _t(a: np.ndarray):
+    return torch.from_numpy(a.view(np.int16) if a.itemsize == 2 else a)
+
+
+def sparse_shard(total, sg, seed, lowp, static_set):
+    """The oracle's seeded shard, loaded into a sparse pool whose static
+    residents are written straight into their HBM homes."""
+    want = O.initialize(total, sg, seed, lowp)
+    nsg = math.ceil(total / sg)
+    opt = D.ShardedOptimizer.allocate(total, sg, lowp=lowp, host_homed=[i for i in range(nsg) if i not in static_set])
+    for a, b in opt.host_runs("state"):
+        opt._p[a:b], opt._m[a:b], opt._v[a:b] = want["p"][a:b], want["m"][a:b], want["v"][a:b]
+    for a, b in opt.host_runs("lowp"):
+        opt._g[a:b], opt._w[a:b] = want["g"][a:b], want["w"][a:b]
+    res = opt.to_device()
+    res.set_static(frozenset(static_set))
+    for i in static_set:
+        g = opt.subgroups[i]
+        for t, key in zip(res.static_views(i), "pmv"):
+            t.copy_(_t(want[key][g.slice]))
+        res.grads.view(torch.int16)[g.slice].copy_(_t(want["g"][g.slice]))
+        res.model16.view(torch.int16)[g.slice].copy_(_t(want["w"][g.slice]))
+    return opt, want
+
+
+def assert_matches(opt, want):
+    assert np.array_equal(opt.params32.view(np.uint32), want["p"].view(np.uint32))
+    assert np.array_equal(opt.momentum32.view(np.uint32), want["m"].view(np.uint32))
+    assert np.array_equal(opt.variance32.view(np.uint32), want["v"].view(np.uint32))
+    assert np.array_equal(opt.model16.view(np.uint16), want["w"].view(np.uint16))
+
+
+@pytest.mark.parametrize("lowp", ["bf16", "fp16"])
+@pytest.mark.parametrize("placement", list(Placement))
+@pytest.mark.parametrize("stride", [1, 2, 3])
+def test_sparse_static_phase_matches_oracle(h100, lowp, placement, stride):
+    total, sg = 10 * (1 << 20) + 12345, 1 << 20  # 11 subgroups, ragged tail, 4 MiB fp32 pieces
+    plan = D.build_plan(11, stride, static_ratio=0.5, placement=placement)
+    opt, want = sparse_shard(total, sg, 5, lowp, plan.static_set)
+    committed = opt.host_bytes
+    assert committed < 16 * total
+    for _ in range(2):
+        D.execute_plan(opt, plan, h100, HYPER)
+        O.sequential_oracle(want)
+    assert opt.host_bytes == committed  # the phase itself commits nothing
+    assert_matches(opt, want)
+
+
+def test_static_set_shrinks_and_grows_between_steps(h100):
+    total, sg = 12 * (1 << 20), 1 << 20
+    ratios = (0.5, 0.25, 0.75, 0.0, 1.0, 0.5)
+    first = D.build_plan(12, 2, static_ratio=ratios[0])
+    opt, want = sparse_shard(total, sg, 8, "bf16", first.static_set)
+    for r in ratios:
+        plan = D.build_plan(12, 2, static_ratio=r, placement=Placement.STATIC_LAST)
+        D.execute_plan(opt, plan, h100, HYPER)
+        O.sequential_oracle(want)
+        assert opt.residency.static_set == plan.static_set
+        assert set(opt.residency.static_sg) == set(plan.static_set)
+    assert_matches(opt, want)
+
+
+def test_sparse_host_io_commits_grads_and_matches(h100):
+    """host_io reads every subgroup's grads from the host image: the target
+    commits the half-precision ranges of the static residents first."""
+    total, sg = 8 * (1 << 20), 1 << 20
+    plan = D.build_plan(8, 2, static_ratio=0.5)
+    opt, want = sparse_shard(total, sg, 2, "bf16", plan.static_set)
+    D.execute_plan(opt, plan, h100, HYPER)  # device grads
+    O.sequential_oracle(want)
+    opt.grads16[:] = want["g"]  # the next step's grads arrive on the host
+    D.execute_plan(opt, plan, h100, HYPER, host_io=True)
+    O.sequential_oracle(want)
+    assert_matches(opt, want)

@@ -364,3 +364,20 @@ def test_refit_profile_from_a_timeline(h100):
     assert prof.channel_params_per_s == pytest.approx(h100.channel_params_per_s, rel=1e-6)
     assert prof.fast_update_params_per_s == pytest.approx(h100.fast_update_params_per_s, rel=1e-6)
     assert prof.cpu_update_params_per_s == pytest.approx(h100.cpu_update_params_per_s, rel=1e-6)
+
+
+def test_capacity_static_ratio():
+    from paper_2410_21316_b200.policy import capacity_static_ratio
+
+    sg = 100_000_000
+    sizes = [sg] * 130  # 13B / 1 rank
+    free = 180 << 30
+    r = capacity_static_ratio(sizes, free)
+    count = D.build_plan(130, 2, static_ratio=r).static_set
+    k = len(count)
+    assert k == int(r * 130 + 1e-9)
+    used = 4 * 13_000_000_000 + 2 * 12 * sg + 12 * sg * k + (4 << 30)
+    assert used <= free < used + 12 * sg  # one more resident would not fit
+    assert capacity_static_ratio([sg] * 70, free) == 1.0  # 7B: every subgroup resident
+    assert capacity_static_ratio([sg] * 10, 1 << 30) == 0.0
+    assert capacity_static_ratio([], free) == 0.0

@@ -171,3 +171,54 @@ def test_emulated_device_ledger():
     for piece in "mvp":
         dev.unstage(0, piece)
     dev.assert_drained()
+
+
+def test_sparse_pool_commits_only_host_homed_subgroups():
+    """allocate(host_homed=...) reserves the shard but commits host memory
+    only for the listed subgroups (2 MB granularity); the rest read as zeros
+    and are committed on demand."""
+    SG = 1 << 20  # 4 MiB of fp32 per subgroup piece
+    opt = D.ShardedOptimizer.allocate(8 * SG, SG, lowp="bf16", host_homed=[0, 1, 5])
+    assert opt.host_runs("state") == [(0, 2 * SG), (5 * SG, 6 * SG)]
+    assert opt.host_runs("lowp") == [(0, 2 * SG), (5 * SG, 6 * SG)]
+    assert [opt.host_committed(i) for i in range(8)] == [True, True, False, False, False, True, False, False]
+    full = 8 * SG * 16
+    assert opt.host_bytes == 3 * SG * 16 < full
+    opt._p[: 2 * SG] = 1.5
+    assert float(opt._p[3 * SG]) == 0.0  # uncommitted range reads as zeros
+    opt.ensure_host([2, 3], "state")
+    assert opt.host_runs("state") == [(0, 4 * SG), (5 * SG, 6 * SG)]
+    assert float(opt._p[0]) == 1.5  # merging runs keeps committed contents
+    opt.ensure_host([2, 3], "state")  # idempotent
+    assert opt.params32.shape == (8 * SG,)  # a full-array read materialises every range
+    assert opt.host_runs("state") == [(0, 8 * SG)]
+    assert all(opt.host_committed(i) for i in range(8))
+    assert float(opt.params32[SG - 1]) == 1.5 and float(opt.params32[7 * SG]) == 0.0
+
+
+def test_sparse_pool_matches_dense_host_oracle():
+    """A sparse shard, fully committed on demand, runs the host oracle to the
+    same digest as a dense one."""
+    dense = D.ShardedOptimizer.initialize(5000, 1024, seed=3, lowp="bf16")
+    sparse = D.ShardedOptimizer.allocate(5000, 1024, lowp="bf16", host_homed=[1, 3])
+    for name in ("params32", "momentum32", "variance32", "model16", "grads16"):
+        getattr(sparse, name)[:] = getattr(dense, name)
+    hyper = D.AdamHyper()
+    D.sequential_oracle(dense, hyper)
+    D.sequential_oracle(sparse, hyper)
+    assert sparse.state_equal(dense)
+    with pytest.raises(ValueError):
+        D.ShardedOptimizer.allocate(5000, 1024, host_homed=[5])
+
+
+def test_sparse_pool_abi_errors():
+    from paper_2410_21316_b200 import _native as N
+
+    hb = N.HostBuffer(1 << 22, sparse=True)
+    assert hb.committed_bytes == 0
+    hb.commit(100, 10)
+    assert hb.committed_bytes == 2 << 20
+    with pytest.raises(ValueError):
+        hb.commit(1 << 22, 1)
+    with pytest.raises(ValueError):
+        N.check(N.lib().dos_host_commit(12345, 0, 1))
