@@ -53,7 +53,8 @@ class DeviceResidency:
         """``grads``/``model16`` may be caller-owned CUDA views (e.g. this
         rank's chunk of a full-model buffer, so the phase writes the model's
         parameters in place); otherwise they are allocated here.  Their
-        current contents are replaced by the host images."""
+        current contents are replaced by the host images (in a sparse pool:
+        where the host range is committed)."""
         torch = _torch()
         if not torch.cuda.is_available():
             raise RuntimeError("no CUDA device visible: the B200 update phase needs a GPU (no CPU fallback)")
@@ -94,14 +95,11 @@ class DeviceResidency:
             src.view(torch.int16 if src.element_size() == 2 else torch.int32), non_blocking=False)
 
     def _h2d_lowp(self, dst, src: np.ndarray) -> None:
-        """Upload a half-precision host array; ranges not committed in a
-        sparse pool read as zeros, so they are zero-filled on the device."""
-        runs = self.opt.host_runs("lowp")
-        if runs == [(0, self.opt.total_params)]:
-            self._h2d(dst, src)
-            return
-        dst.zero_()
-        for a, b in runs:
+        """Upload a half-precision host array.  In a sparse pool only the
+        committed ranges have a host image; elsewhere the device copy is the
+        only one and is left as it is (it is pulled to the host if the range
+        is ever committed, ``on_host_commit``)."""
+        for a, b in self.opt.host_runs("lowp"):
             self._h2d(dst[a:b], src[a:b])
 
     def _d2h_lowp(self, dst: np.ndarray, src) -> None:

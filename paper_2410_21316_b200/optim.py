@@ -46,7 +46,7 @@ from .state import ShardedOptimizer, lowp_downscale
 
 class DeepOptimizerStates:
     def __init__(self, params, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 0.0,
-                 *, subgroup_size: int = 100_000_000, profile=None, stride="auto", static_ratio: float = 0.0,
+                 *, subgroup_size: int = 100_000_000, profile=None, stride="auto", static_ratio=0.0,
                  master_params=None, process_group=None, average_grads: bool = False, explore: int = 3,
                  fused_gather: bool = True, fused_reduce: bool = True) -> None:
         import torch
@@ -83,23 +83,42 @@ class DeepOptimizerStates:
                 p.grad = self.flat_grad[off:off + n].view(p.shape)
                 off += n
 
-        opt = ShardedOptimizer.allocate(mine, sg, lowp=self.lowp)
+        sizes = [g.size for g in lay.ranks[self.rank]]
+        if static_ratio == "auto":
+            # capacity-aware: as many subgroups homed in HBM as fit beside two
+            # windows (the grads and working copy already live in the flat buffers)
+            r = policy.capacity_static_ratio(sizes, torch.cuda.mem_get_info(dev)[0], lowp_bytes_per_param=0)
+            static_ratio = -self._max_over_ranks(-r) if self.world > 1 else r  # same plan shape everywhere
+        static = build_plan(len(sizes), 1, static_ratio=static_ratio).static_set
+        # sparse pinned pool: host memory only for the host-homed subgroups
+        opt = ShardedOptimizer.allocate(mine, sg, lowp=self.lowp,
+                                        host_homed=[i for i in range(len(sizes)) if i not in static])
         chunk = self.flat[self.offset:self.offset + mine]
         if master_params is None:
-            torch.from_numpy(opt._p).copy_(chunk.float())  # exact widening
+            p32 = chunk.float()  # exact widening
         else:
             flat_m = torch.cat([m.detach().reshape(-1).float().cpu() for m in master_params])
             if flat_m.numel() != total:
                 raise ValueError("master_params must match params element for element")
-            opt._p[:] = flat_m[self.offset:self.offset + mine].numpy()
+            m32 = flat_m[self.offset:self.offset + mine].contiguous()
             with torch.no_grad():  # working copy = RNE of the masters
-                chunk.copy_(torch.from_numpy(lowp_downscale(opt._p, self.lowp).view(np.int16)).view(dt))
-        opt._w[:] = chunk.view(torch.int16).cpu().numpy().view(opt._w.dtype)
-        opt._m[:] = 0
-        opt._v[:] = 0
-        opt._g[:] = 0
+                chunk.copy_(torch.from_numpy(lowp_downscale(m32.numpy(), self.lowp).view(np.int16)).view(dt))
+            p32 = m32.to(dev)
+        w16 = chunk.view(torch.int16)
+        for a, b in opt.host_runs("state"):
+            torch.from_numpy(opt._p[a:b]).copy_(p32[a:b])
+            opt._m[a:b] = 0
+            opt._v[a:b] = 0
+        for a, b in opt.host_runs("lowp"):
+            torch.from_numpy(opt._w[a:b].view(np.int16)).copy_(w16[a:b])
+            opt._g[a:b] = 0
         self.opt = opt
         self.res = opt.to_device(dev, grads=self.flat_grad[self.offset:self.offset + mine], model16=chunk)
+        self.res.set_static(static)  # residents start zeroed (m, v) ...
+        for i in sorted(static):
+            g = opt.subgroups[i]
+            self.res.static_views(i)[0].copy_(p32[g.start:g.stop])  # ... with their masters in HBM
+        del p32
         self.coll = BucketedCollectives(lay, process_group) if self.world > 1 else None
         # fused all-gather: K1 writes the working copy straight into every
         # peer's full-model buffer (IPC-mapped); else bucketed overlapped gathers
@@ -113,7 +132,7 @@ class DeepOptimizerStates:
             profile = get_profile("b200-node")
         self.profile = profile
         self.static_ratio = static_ratio
-        self.sizes = [g.size for g in opt.subgroups]
+        self.sizes = sizes
         self.tuner = None
         if stride == "auto":
             self.tuner = policy.StrideTuner(profile, self.sizes, range(1, 7), static_ratio, explore=explore)
@@ -163,7 +182,7 @@ class DeepOptimizerStates:
 
         t = torch.tensor([x], dtype=torch.float64)
         if dist.get_backend(self.group) == "nccl":
-            t = t.to(self.res.device)
+            t = t.to(self.params[0].device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
         return float(t.item())
 
@@ -213,6 +232,9 @@ class DeepOptimizerStates:
     def load_state_dict(self, sd: dict) -> None:
         if (sd.get("rank", 0), sd.get("world", 1)) != (self.rank, self.world):
             raise ValueError("state dict belongs to another rank / world size")
+        n = len(self.opt.subgroups)
+        self.opt.ensure_host(range(n), "state")  # a sparse pool: every range gets a host image
+        self.opt.ensure_host(range(n), "lowp")
         self.res.sync_all_host()
         self.opt._p[:] = sd["params32"]
         self.opt._m[:] = sd["momentum32"]

@@ -20,11 +20,12 @@ def _model():
 
 
 @pytest.mark.parametrize("stride", [1, 2, 3])
-def test_training_steps_match_oracle(stride):
+@pytest.mark.parametrize("static_ratio", [0.2, "auto"])
+def test_training_steps_match_oracle(stride, static_ratio):
     model = _model()
     masters = torch.cat([p.detach().float().reshape(-1).cpu() for p in model.parameters()]).numpy().copy()
     opt = DeepOptimizerStates(model.parameters(), lr=1e-3, subgroup_size=20_000, profile=get_profile("h100-node"),
-                              stride=stride, static_ratio=0.2)
+                              stride=stride, static_ratio=static_ratio)
     total = masters.size
     st = {"p": masters.copy(), "m": np.zeros(total, np.float32), "v": np.zeros(total, np.float32),
           "w": O.bf16_from_f32(masters), "g": None, "subgroups": O.shard_subgroups(total, 20_000), "step": 0,
@@ -42,3 +43,25 @@ def test_training_steps_match_oracle(stride):
         assert got.view(np.uint16).tobytes() == st["w"].tobytes()
         assert opt.master_params().tobytes() == st["p"].tobytes()
     assert opt.step_count == 3
+
+
+def test_capacity_aware_state_dict_roundtrip():
+    """static_ratio="auto" homes the whole (small) shard in HBM with no host
+    state; state_dict/load_state_dict still round-trip it exactly."""
+    model = _model()
+    opt = DeepOptimizerStates(model.parameters(), subgroup_size=20_000, profile=get_profile("h100-node"),
+                              stride=2, static_ratio="auto")
+    assert opt.static_ratio == 1.0 and opt.opt.host_bytes == 0
+    x = torch.randn(32, 256, device="cuda", dtype=torch.bfloat16)
+    for _ in range(2):
+        opt.zero_grad()
+        model(x).float().pow(2).mean().backward()
+        opt.step()
+    sd = opt.state_dict()
+    before = torch.cat([p.detach().reshape(-1) for p in model.parameters()]).clone()
+    opt.load_state_dict(sd)
+    after = torch.cat([p.detach().reshape(-1) for p in model.parameters()])
+    assert torch.equal(before.view(torch.int16), after.view(torch.int16))
+    sd2 = opt.state_dict()
+    for k in ("params32", "momentum32", "variance32"):
+        assert sd2[k].tobytes() == sd[k].tobytes()

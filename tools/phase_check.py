@@ -8,8 +8,8 @@ from bench import fill_shard
 P, SG = 7_000_000_000, 100_000_000
 dev = torch.device("cuda", 0)
 opt = D.ShardedOptimizer.allocate(P, SG, lowp="bf16")
-fill_shard(opt, 7, dev)
 opt.to_device(dev)
+fill_shard(opt, 7, dev)
 print(json.dumps({"h1_alone": profile_b200.measure_h1(100_000_000), "h1_dma": profile_b200.measure_h1(100_000_000, with_dma=True)}))
 prof = profile_b200.measure_profile(quick=True)
 hyper = D.AdamHyper()

@@ -11,8 +11,8 @@ P = int(float(sys.argv[1])) if len(sys.argv) > 1 else 7_000_000_000
 SG = 100_000_000
 dev = torch.device("cuda", 0)
 opt = D.ShardedOptimizer.allocate(P, SG, lowp="bf16")
-fill_shard(opt, 7, dev)
 opt.to_device(dev)
+fill_shard(opt, 7, dev)
 prof = profile_b200.measure_profile(quick=True)
 hyper = D.AdamHyper()
 n = len(opt.subgroups)
