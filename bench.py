@@ -255,7 +255,10 @@ class B200Bench:
                 dist.init_process_group("nccl", device_id=self.device)
             else:
                 dist.init_process_group("gloo")
-            D._native.lib().dos_set_host_threads(max(1, len(os.sched_getaffinity(0)) // world))
+            # each rank's H1 team on its own share of the host cores (its GPU's NUMA node)
+            from paper_2410_21316_b200.distributed import bind_host_cores
+
+            self.cores = bind_host_cores(local, int(os.environ.get("LOCAL_WORLD_SIZE", world)))
         if args.host_threads > 0:
             D._native.lib().dos_set_host_threads(args.host_threads)
         self.P, self.SG = int(args.params), int(args.subgroup)

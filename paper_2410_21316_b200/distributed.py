@@ -309,3 +309,75 @@ def finalising_actions(plan) -> dict[int, int]:
         elif a.kind is ActionKind.H2D_PARAMS16 and plan.devices[a.subgroup] is Device.CPU:
             out[a.subgroup] = a.id
     return out
+
+
+# ---------------------------------------------------------------- host cores per rank
+
+
+def plan_core_binding(allowed, gpu_nodes, node_cpus, local_rank: int) -> list[int]:
+    """The host cores rank ``local_rank`` should run H1 on, when every local
+    rank's process starts with the same affinity mask (torchrun).
+
+    ``gpu_nodes[r]``: NUMA node of local rank r's GPU (-1 unknown);
+    ``node_cpus[node]``: that node's CPUs.  Ranks whose GPUs sit on the same
+    node split that node's allowed CPUs into equal contiguous slices (the
+    paper pins each rank's CPU optimizer work to its socket, §8(e)); without
+    NUMA information the allowed CPUs are split evenly across all ranks."""
+    allowed = sorted(set(allowed))
+    world = len(gpu_nodes)
+    if world <= 1:
+        return allowed
+    node = gpu_nodes[local_rank]
+    pool = [c for c in allowed if c in set(node_cpus.get(node, ()))] if node >= 0 else []
+    peers = [r for r in range(world) if gpu_nodes[r] == node] if pool else list(range(world))
+    if not pool:
+        pool = allowed
+    k, i = len(peers), peers.index(local_rank)
+    if len(pool) < k:  # fewer cores than ranks: share round-robin
+        return [pool[i % len(pool)]]
+    per = len(pool) // k
+    return pool[i * per:(i + 1) * per]
+
+
+def _parse_cpulist(text: str) -> list[int]:
+    out: list[int] = []
+    for part in text.strip().split(","):
+        if not part:
+            continue
+        a, _, b = part.partition("-")
+        out.extend(range(int(a), int(b or a) + 1))
+    return out
+
+
+def bind_host_cores(local_rank: int, local_world: int) -> list[int]:
+    """Restrict this process (and libdos's H1 team) to its share of the host
+    cores: the CPUs of its GPU's NUMA node, split among the local ranks on
+    that node.  Returns the CPUs chosen."""
+    import os
+
+    import torch
+
+    from . import _native as N
+
+    def gpu_node(i: int) -> int:
+        try:
+            p = torch.cuda.get_device_properties(i)
+            bus = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            with open(f"/sys/bus/pci/devices/{bus}/numa_node") as fh:
+                return int(fh.read().strip())
+        except Exception:
+            return -1
+
+    nodes = [gpu_node(i) for i in range(local_world)] if torch.cuda.device_count() >= local_world else [-1] * local_world
+    node_cpus: dict[int, list[int]] = {}
+    for nd in set(nodes):
+        if nd >= 0:
+            try:
+                with open(f"/sys/devices/system/node/node{nd}/cpulist") as fh:
+                    node_cpus[nd] = _parse_cpulist(fh.read())
+            except OSError:
+                pass
+    cpus = plan_core_binding(os.sched_getaffinity(0), nodes, node_cpus, local_rank)
+    os.sched_setaffinity(0, cpus)
+    N.lib().dos_set_host_threads(len(cpus))  # rebuilds the team inside the new mask
+    return cpus

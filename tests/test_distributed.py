@@ -117,3 +117,24 @@ def test_sharded_update_then_gather_equals_single_rank():
     for p in procs:
         p.join(timeout=60)
     assert all(ok for _, ok in res), res
+
+
+def test_plan_core_binding():
+    from paper_2410_21316_b200.distributed import _parse_cpulist, plan_core_binding
+
+    assert _parse_cpulist("0-3,8,10-11\n") == [0, 1, 2, 3, 8, 10, 11]
+    allowed = range(32)
+    nodes = {0: list(range(16)), 1: list(range(16, 32))}
+    # 8 GPUs, 4 per socket: each rank gets 4 cores of its own socket, disjoint
+    gpu_nodes = [0, 0, 0, 0, 1, 1, 1, 1]
+    got = [plan_core_binding(allowed, gpu_nodes, nodes, r) for r in range(8)]
+    assert got[0] == [0, 1, 2, 3] and got[5] == [20, 21, 22, 23]
+    assert sorted(c for g in got for c in g) == list(range(32))
+    # no NUMA information: an even split of the allowed set
+    got = [plan_core_binding(range(16), [-1] * 4, {}, r) for r in range(4)]
+    assert got == [[0, 1, 2, 3], [4, 5, 6, 7], [8, 9, 10, 11], [12, 13, 14, 15]]
+    # fewer cores than ranks, and a single rank keeps everything
+    assert plan_core_binding([0, 1], [-1] * 4, {}, 3) == [1]
+    assert plan_core_binding(range(8), [0], nodes, 0) == list(range(8))
+    # a node whose CPUs are outside the allowed mask falls back to the mask
+    assert plan_core_binding(range(4), [2, 2], {2: [40, 41]}, 1) == [2, 3]
