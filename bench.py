@@ -54,6 +54,9 @@ def parse():
                     help="fraction of subgroups whose fp32 state stays in HBM (TwinFlow-style residents); 0.2 is "
                          "the paper's representative setting (PAPER.md:631-635); the rest is host-offloaded. 'auto': as many "
                          "as fit in HBM (capacity-aware)")
+    ap.add_argument("--placement", default="static_first", choices=["static_first", "static_last"],
+                    help="where the static residents sit in the plan (scheduler.py:161-168); static_first lets "
+                         "their updates lead the fast lane (with host buffers their grads arrive first)")
     ap.add_argument("--capacity-gb", type=float, default=None,
                     help="imposed dynamic fast-tier budget (default: two windows)")
     ap.add_argument("--cpu-sample", type=int, default=70,
@@ -326,7 +329,8 @@ class B200Bench:
             self.static_ratio = -self.max_over_ranks(-ratio)  # same plan shape on every rank
         else:
             self.static_ratio = float(a.static_ratio)
-        static = D.build_plan(self.nsg, 1, static_ratio=self.static_ratio).static_set
+        self.placement = D.Placement(a.placement)
+        static = D.build_plan(self.nsg, 1, static_ratio=self.static_ratio, placement=self.placement).static_set
         t0 = time.perf_counter()
         # sparse pinned pool: host memory only for the host-homed subgroups
         self.opt = D.ShardedOptimizer.allocate(self.P_rank, self.SG, lowp=a.lowp,
@@ -354,7 +358,7 @@ class B200Bench:
             stride = D.ALL_CPU
         else:
             stride = int(a.stride)
-        self.plan = D.build_plan(self.nsg, stride, static_ratio=self.static_ratio)
+        self.plan = D.build_plan(self.nsg, stride, static_ratio=self.static_ratio, placement=self.placement)
         if a.stride == "auto":
             r = D.execute_plan(self.opt, self.plan, self.profile, self.hyper)
             self.profile = self.broadcast(self.policy.refit_profile(self.profile, r.measured, self.sizes))
@@ -367,7 +371,7 @@ class B200Bench:
     def host_fits(self, ratio: float) -> bool:
         """Would homing every non-static subgroup on the host (16 B/param
         pinned) fit in the host memory still available?"""
-        static = self.D.build_plan(self.nsg, 1, static_ratio=ratio).static_set
+        static = self.D.build_plan(self.nsg, 1, static_ratio=ratio, placement=self.placement).static_set
         need = 16 * sum(s for i, s in enumerate(self.sizes) if i not in static)
         ok = need <= self.opt.host_bytes + host_available_bytes() - (8 << 30)
         return -self.max_over_ranks(-1.0 if ok else 0.0) >= 1.0
@@ -376,7 +380,7 @@ class B200Bench:
         D = self.D
         slowdown = float(self.broadcast(self.profile_b200.LAST_RAW.get("link_slowdown_under_h1", 1.0)))
         tuner = self.policy.StrideTuner(self.profile, self.sizes, range(1, 7), ratio, explore=explore,
-                                        link_slowdown=slowdown)
+                                        link_slowdown=slowdown, placement=self.placement)
         tuner.queue = list(self.broadcast(tuner.queue))  # same exploration order on every rank
         while tuner.exploring:
             k = tuner.next_stride()
@@ -507,7 +511,8 @@ class B200Bench:
             # host buffers shift the link/host balance (grads H2D and the working
             # copy D2H for fast subgroups, no grad flush for host ones): re-tune
             # the stride for this mode, hill-climbing from the device-mode choice
-            tuner = self.policy.StrideTuner(self.profile, self.sizes, range(1, 7), self.static_ratio, explore=1)
+            tuner = self.policy.StrideTuner(self.profile, self.sizes, range(1, 7), self.static_ratio, explore=1,
+                                            placement=self.placement)
             tuner.queue = [plan.stride]
             while tuner.exploring:
                 k = tuner.next_stride()
@@ -519,6 +524,7 @@ class B200Bench:
         last = []
         ms = self.timed(lambda: last.append(D.execute_plan(opt, plan, self.profile, self.hyper, host_io=True)),
                         self.args.steps)
+        self.e2e_result = last[-1]
         ev = last[-1].timeline.events  # the plan's link bytes (SimTarget.bytes_of), + host_io's 2+2 B per fast param
         h2d_b = sum(e.bytes for e in ev if e.action.lane.value == "h2d")
         d2h_b = sum(e.bytes for e in ev if e.action.lane.value == "d2h")
@@ -694,7 +700,10 @@ class B200Bench:
 
         os.makedirs(self.args.trace_dir, exist_ok=True)
         tag = f"{self.P / 1e9:g}B_stride{self.stride}"
-        for kind, tl in (("measured", self.results[-1].measured), ("predicted", self.results[-1].timeline)):
+        runs = [("measured", self.results[-1].measured), ("predicted", self.results[-1].timeline)]
+        if getattr(self, "e2e_result", None) is not None and self.e2e_result.measured is not None:
+            runs.append(("measured_e2e", self.e2e_result.measured))
+        for kind, tl in runs:
             with open(os.path.join(self.args.trace_dir, f"{kind}_{tag}.csv"), "w") as fh:
                 write_trace_csv(tl, fh)
 
@@ -714,7 +723,7 @@ class B200Bench:
             "planner_k": "all_cpu" if self.choice.k is D.ALL_CPU else self.choice.k, "k_real": self.choice.k_real,
             "predicted_span_ms_by_stride": None if self.stride_spans is None else
             {str(k): v / 1e6 for k, v in self.stride_spans.items()},
-            "measured_span_ms_by_stride": self.tuned, "static_ratio": r,
+            "measured_span_ms_by_stride": self.tuned, "static_ratio": r, "placement": self.placement.value,
             "fast_capacity_bytes": self.cap, "hbm_windows": windows,
             "parallelism": f"zero3-shard{self.world}", "l2": "inputs > L2 (28 B/param over 1e8-param subgroups)"}
         line = {"metric": METRIC, "value": self.P / (self.ms * 1e-3), "unit": UNIT, "n_gpus": self.world,

@@ -67,7 +67,8 @@ struct Job {
 struct Engine {
   int dev = 0;
   cudaStream_t st[3] = {nullptr, nullptr, nullptr};  // fast, h2d, d2h
-  cudaStream_t gst = nullptr;                        // in-phase grad flush (D2H)
+  cudaStream_t gst = nullptr;                        // in-phase grad flush (D2H); host_io: residents' grads H2D
+  cudaStream_t ost = nullptr;                        // host_io: residents' working copy D2H
   std::vector<cudaEvent_t> ev_g;                      // per action: its grads are on the host
   std::vector<cudaEvent_t> ev_sg;                     // per subgroup: host_io grads of a static resident landed
   int nslots = 0;
@@ -362,10 +363,11 @@ struct Engine {
         if (!a->is_static && !(sg_slot[sg] >= 0 && (sg_mask[sg] & (1u << PIECE_P))))
           return dos_set_error(DOS_ESTATE, "FLUSH_OUT_MODEL16 of subgroup %d without staged params", sg);
         if (S.host_io && a->is_static) {
-          // mirror a resident's working copy on the side stream, off the compute lane
+          // mirror a resident's working copy on its own side stream, off the
+          // compute lane and not queued behind the residents' grads H2D (gst)
           DOS_CU(cudaEventRecord(ev_sg[sg], s));
-          DOS_CU(cudaStreamWaitEvent(gst, ev_sg[sg], 0));
-          DOS_CU(copy_lowp_d2h(start, n, gst));
+          DOS_CU(cudaStreamWaitEvent(ost, ev_sg[sg], 0));
+          DOS_CU(copy_lowp_d2h(start, n, ost));
         }
         return DOS_OK;
       case DOS_FLUSH_OUT_M:
@@ -478,6 +480,7 @@ struct Engine {
     DOS_CU(cudaStreamWaitEvent(st[1], ev0, 0));
     DOS_CU(cudaStreamWaitEvent(st[2], ev0, 0));
     DOS_CU(cudaStreamWaitEvent(gst, ev0, 0));
+    DOS_CU(cudaStreamWaitEvent(ost, ev0, 0));
     if (S.host_io) {
       // static residents' grads go H2D first thing, on the side stream, so
       // their updates (STATIC_LAST: at the end of the phase) never wait on them
@@ -506,8 +509,8 @@ struct Engine {
     }
     active = false;
     cudaError_t ce = cudaSuccess;
-    for (int i = 0; i < 4; ++i) {
-      cudaError_t e = cudaStreamSynchronize(i < 3 ? st[i] : gst);
+    for (int i = 0; i < 5; ++i) {
+      cudaError_t e = cudaStreamSynchronize(i < 3 ? st[i] : i == 3 ? gst : ost);
       if (e != cudaSuccess && ce == cudaSuccess) ce = e;
     }
     if (ce != cudaSuccess) return dos_set_error(DOS_ECUDA, "update phase failed on the device: %s", cudaGetErrorString(ce));
@@ -543,6 +546,7 @@ struct Engine {
     DOS_CU(cudaSetDevice(dev));
     for (int i = 0; i < 3; ++i) DOS_CU(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking));
     DOS_CU(cudaStreamCreateWithFlags(&gst, cudaStreamNonBlocking));
+    DOS_CU(cudaStreamCreateWithFlags(&ost, cudaStreamNonBlocking));
     DOS_CU(cudaEventCreate(&ev0));
     if (slot_elems > 0) DOS_CU(cudaMalloc(reinterpret_cast<void**>(&slot_mem), (size_t)nslots * 3 * slot_elems * 4));
     cudaDriverEntryPointQueryResult qr;
@@ -569,10 +573,11 @@ struct Engine {
         cudaStreamSynchronize(st[i]);
         cudaStreamDestroy(st[i]);
       }
-    if (gst) {
-      cudaStreamSynchronize(gst);
-      cudaStreamDestroy(gst);
-    }
+    for (cudaStream_t side : {gst, ost})
+      if (side) {
+        cudaStreamSynchronize(side);
+        cudaStreamDestroy(side);
+      }
     for (auto e : ev_s) cudaEventDestroy(e);
     for (auto e : ev_e) cudaEventDestroy(e);
     for (auto e : ev_g) cudaEventDestroy(e);

@@ -19,7 +19,7 @@ import dataclasses
 from typing import Iterable, Sequence
 
 from .perfmodel import ALL_CPU
-from .plan import ActionKind, Device, Lane, ScheduledAction, UpdatePlan, build_plan
+from .plan import ActionKind, Device, Lane, Placement, ScheduledAction, UpdatePlan, build_plan
 from .state import SystemProfile
 from .timing import SimTarget, Timeline, build_timeline, normalize_sizes
 
@@ -64,14 +64,14 @@ def refit_profile(profile: SystemProfile, measured: Timeline, sizes: Sequence[in
     return dataclasses.replace(profile, **upd)
 
 
-def _quiet_plan(n: int, stride, static_ratio: float) -> UpdatePlan:
+def _quiet_plan(n: int, stride, static_ratio: float, placement: Placement = Placement.STATIC_LAST) -> UpdatePlan:
     """build_plan without the all-static warning (the policy sweeps ratios
     up to 1.0 on purpose; the stride is then irrelevant, not a mistake)."""
     import warnings
 
     with warnings.catch_warnings():
         warnings.simplefilter("ignore", UserWarning)
-        return build_plan(n, stride, static_ratio=static_ratio)
+        return build_plan(n, stride, static_ratio=static_ratio, placement=placement)
 
 
 _LINK_KINDS = frozenset({ActionKind.PREFETCH_M, ActionKind.PREFETCH_V, ActionKind.PREFETCH_P,
@@ -158,13 +158,21 @@ class StrideTuner:
     model's ranking is off by more than the explored set.  Decisions depend
     only on the recorded spans, so ranks that record the same (max-over-
     ranks) spans stay in lockstep.
+
+    ``placement`` is the plan's static placement (scheduler.py:161-168).
+    With host buffers (``execute_plan(host_io=True)``) the residents' grads
+    stream in from the host at the start of the phase, so STATIC_FIRST lets
+    their updates — and the working-copy D2H behind them — lead the fast lane
+    instead of queueing behind the streamed subgroups' prefetches.
     """
 
     def __init__(self, profile: SystemProfile, sizes: Sequence[int], candidates: Iterable = range(1, 7),
                  static_ratio: float = 0.0, explore: int = 4, num_slots: int = 2,
-                 link_slowdown: float = 1.0, hill_climb: bool = True) -> None:
+                 link_slowdown: float = 1.0, hill_climb: bool = True,
+                 placement: Placement = Placement.STATIC_LAST) -> None:
         self.sizes = list(sizes)
         self.static_ratio = static_ratio
+        self.placement = placement
         best, spans = choose_stride(profile, self.sizes, candidates, static_ratio, num_slots, link_slowdown)
         ranked = sorted(spans, key=lambda k: spans[k])
         self.queue = ranked[:max(1, explore)]
@@ -195,7 +203,7 @@ class StrideTuner:
         return self.plan_for(self.next_stride())
 
     def plan_for(self, stride) -> UpdatePlan:
-        return _quiet_plan(len(self.sizes), stride, self.static_ratio)
+        return _quiet_plan(len(self.sizes), stride, self.static_ratio, self.placement)
 
 
 def fast_fraction(plan: UpdatePlan, sizes: Sequence[int]) -> float:
