@@ -218,6 +218,12 @@ typedef struct dos_state_desc {
    * (static_offset[i] >= 0 still marks residency), so the static set can
    * grow and shrink one subgroup at a time without re-packing HBM. */
   float* const* dev_static_sg;
+  /* host_io only: 0 ships every static resident's grads H2D at phase start
+   * (best when the residents' updates come last); k > 0 issues each
+   * resident's grads when its GPU_UPDATE is submitted, k resident updates
+   * ahead of the fast lane, so the copy engine interleaves them with the
+   * H2D lane instead of draining them all first (best when they lead). */
+  int32_t host_io_ahead;
 } dos_state_desc;
 
 #define DOS_MAX_PEERS 7

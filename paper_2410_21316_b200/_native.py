@@ -63,6 +63,7 @@ class dos_state_desc(C.Structure):
         ("src_g", C.POINTER(C.c_void_p)),
         ("grad_scale", C.c_float),
         ("dev_static_sg", C.POINTER(C.c_void_p)),
+        ("host_io_ahead", C.c_int32),
     ]
 
 

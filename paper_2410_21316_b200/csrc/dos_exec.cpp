@@ -71,6 +71,7 @@ struct Engine {
   cudaStream_t ost = nullptr;                        // host_io: residents' working copy D2H
   std::vector<cudaEvent_t> ev_g;                      // per action: its grads are on the host
   std::vector<cudaEvent_t> ev_sg;                     // per subgroup: host_io grads of a static resident landed
+  std::deque<int32_t> static_q;                       // host_io_ahead: resident updates whose grads are in flight
   int nslots = 0;
   int64_t slot_elems = 0;
   float* slot_mem = nullptr;
@@ -342,8 +343,21 @@ struct Engine {
         if (a->is_static) {
           const int64_t o = static_off[sg];
           if (o < 0) return dos_set_error(DOS_ESTATE, "subgroup %d marked static but has no HBM residence", sg);
-          // host_io: its grads were shipped H2D at phase start on the side stream
-          if (S.host_io) DOS_CU(cudaStreamWaitEvent(s, ev_sg[sg], 0));
+          if (S.host_io) {
+            if (S.host_io_ahead > 0) {
+              // ship this resident's grads now, at most host_io_ahead resident
+              // updates ahead of the fast lane
+              if ((int)static_q.size() >= S.host_io_ahead) {
+                DOS_CU(cudaStreamWaitEvent(gst, ev_s[static_q.front()], 0));
+                static_q.pop_front();
+              }
+              DOS_CU(copy_grads_h2d(start, n, gst));
+              DOS_CU(cudaEventRecord(ev_sg[sg], gst));
+              static_q.push_back(a->id);
+            }
+            // (host_io_ahead == 0: shipped H2D at phase start on the side stream)
+            DOS_CU(cudaStreamWaitEvent(s, ev_sg[sg], 0));
+          }
           float* sp = S.dev_static_sg ? S.dev_static_sg[3 * sg] : S.dev_static_p + o;
           float* sm = S.dev_static_sg ? S.dev_static_sg[3 * sg + 1] : S.dev_static_m + o;
           float* sv = S.dev_static_sg ? S.dev_static_sg[3 * sg + 2] : S.dev_static_v + o;
@@ -489,7 +503,8 @@ struct Engine {
         DOS_CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         ev_sg.push_back(e);
       }
-      for (int i = 0; i < ns; ++i)
+      static_q.clear();
+      for (int i = 0; i < ns && S.host_io_ahead <= 0; ++i)
         if (static_off[i] >= 0) {
           DOS_CU(copy_grads_h2d(sg_start[i], sg_size[i], gst));
           DOS_CU(cudaEventRecord(ev_sg[i], gst));

@@ -243,7 +243,7 @@ class DeviceResidency:
         return eng
 
     def state_desc(self, host_io: bool = False, peers=None, flush_grads: bool = False,
-                   grad_sources=None) -> tuple[N.dos_state_desc, list]:
+                   grad_sources=None, host_io_ahead: int = 0) -> tuple[N.dos_state_desc, list]:
         """``peers``: addresses (ints) where this shard starts in each peer's
         full-model buffer — the fused all-gather targets (include/dos.h).
         ``grad_sources``: a ``distributed.GradSources`` (fused reduce-scatter)."""
@@ -269,6 +269,7 @@ class DeviceResidency:
             dev_g=self.grads.data_ptr(), dev_lowp=self.model16.data_ptr(),
             dev_static_p=None, dev_static_m=None, dev_static_v=None,
             dev_static_sg=C.cast(self._static_ptrs, C.POINTER(C.c_void_p)),
+            host_io_ahead=host_io_ahead,
             host_io=1 if host_io else 0,
             npeers=len(peers),
             peer_lowp=C.cast(peer_arr, C.POINTER(C.c_void_p)),
@@ -397,7 +398,11 @@ class B200Target(SimTarget):
         self._submitted = 0
 
     def _begin(self) -> None:
-        desc, keep = self.residency.state_desc(self.host_io, self.peers, self.flush_grads, self.grad_sources)
+        # with host buffers, residents that lead the fast lane get their grads
+        # just ahead of it; residents that trail it get them all at phase start
+        first_fast = next((a.subgroup for a in self.plan.actions if a.kind.value == "gpu_update"), None)
+        ahead = 2 if (self.host_io and first_fast is not None and first_fast in self.plan.static_set) else 0
+        desc, keep = self.residency.state_desc(self.host_io, self.peers, self.flush_grads, self.grad_sources, ahead)
         self._keep = (desc, keep)
         h = self.hyper
         bc1, bc2 = bias_corrections(h.beta1, h.beta2, self.step)

@@ -81,11 +81,14 @@ def test_static_set_shrinks_and_grows_between_steps(h100):
     assert_matches(opt, want)
 
 
-def test_sparse_host_io_commits_grads_and_matches(h100):
+@pytest.mark.parametrize("placement", list(Placement))
+def test_sparse_host_io_commits_grads_and_matches(h100, placement):
     """host_io reads every subgroup's grads from the host image: the target
-    commits the half-precision ranges of the static residents first."""
+    commits the half-precision ranges of the static residents first.  With
+    STATIC_FIRST the residents' grads are shipped just ahead of the fast lane
+    (host_io_ahead), with STATIC_LAST all at phase start."""
     total, sg = 8 * (1 << 20), 1 << 20
-    plan = D.build_plan(8, 2, static_ratio=0.5)
+    plan = D.build_plan(8, 2, static_ratio=0.5, placement=placement)
     opt, want = sparse_shard(total, sg, 2, "bf16", plan.static_set)
     D.execute_plan(opt, plan, h100, HYPER)  # device grads
     O.sequential_oracle(want)
