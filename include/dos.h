@@ -135,6 +135,10 @@ int dos_host_reserve(size_t bytes, int numa_node, int register_cuda, void** out)
 int dos_host_commit(void* base, size_t offset, size_t len);
 int64_t dos_host_committed(void* base);
 int dos_host_threads(void); /* size of the library's host team */
+/* Host memory probe (the host-DRAM roofline's denominator): one pass of the
+ * team over `bytes`, reading src (mode 0) or copying src -> dst (mode 1);
+ * the pass's wall seconds in *seconds.  Not on the update path. */
+int dos_host_membw(const void* src, void* dst, size_t bytes, int mode, int nthreads, double* seconds);
 int dos_set_host_threads(int n);
 
 /* ---- the copy-stream / host-lane engine ---------------------------------

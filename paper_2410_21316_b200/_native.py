@@ -111,6 +111,7 @@ SIGNATURES: dict[str, tuple] = {
     "dos_host_commit": (_I, [_VP, _SZ, _SZ]),
     "dos_host_committed": (C.c_int64, [_VP]),
     "dos_host_threads": (_I, []),
+    "dos_host_membw": (_I, [_VP, _VP, _SZ, _I, _I, C.POINTER(C.c_double)]),
     "dos_set_host_threads": (_I, [_I]),
     "dos_exec_create": (_I, [C.POINTER(dos_exec_config), C.POINTER(_VP)]),
     "dos_exec_destroy": (_I, [_VP]),

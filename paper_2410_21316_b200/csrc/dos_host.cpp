@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <functional>
 #include <mutex>
@@ -237,6 +238,39 @@ extern "C" int dos_upscale_host(const void* x, int in_dtype, float* out, int64_t
   if (!x || !out) return dos_set_error(DOS_EINVAL, "NULL buffer");
   const dos_hk_table& t = hk();
   parallel_chunks(n, nthreads, [&](int64_t lo, int64_t hi) { t.up(x, in_dtype, out, lo, hi); });
+  return DOS_OK;
+}
+
+// ---------------------------------------------------------------- host memory probe
+static volatile uint64_t g_membw_sink;
+// The host-DRAM roofline's denominator: one pass of the team over a buffer,
+// reading it (mode 0) or copying it (mode 1, glibc memcpy: non-temporal
+// stores at these sizes).  Seconds of the pass in *seconds.
+extern "C" int dos_host_membw(const void* src, void* dst, size_t bytes, int mode, int nthreads, double* seconds) {
+  if (!src || !seconds || (mode == 1 && !dst) || mode < 0 || mode > 1)
+    return dos_set_error(DOS_EINVAL, "dos_host_membw: bad arguments");
+  const int64_t lines = (int64_t)(bytes / 64);
+  std::atomic<uint64_t> sink{0};
+  const auto t0 = std::chrono::steady_clock::now();
+  parallel_chunks(lines, nthreads, [&](int64_t lo, int64_t hi) {
+    const char* s = static_cast<const char*>(src) + lo * 64;
+    const size_t n = (size_t)(hi - lo) * 64;
+    if (mode == 1) {
+      memcpy(static_cast<char*>(dst) + lo * 64, s, n);
+      return;
+    }
+    const uint64_t* q = reinterpret_cast<const uint64_t*>(s);
+    uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    for (size_t i = 0; i + 4 <= n / 8; i += 4) {
+      a0 ^= q[i];
+      a1 ^= q[i + 1];
+      a2 ^= q[i + 2];
+      a3 ^= q[i + 3];
+    }
+    sink.fetch_xor(a0 ^ a1 ^ a2 ^ a3, std::memory_order_relaxed);
+  });
+  *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  g_membw_sink = sink.load();  // keeps the reads observable
   return DOS_OK;
 }
 

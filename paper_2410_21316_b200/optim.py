@@ -48,7 +48,11 @@ class DeepOptimizerStates:
     def __init__(self, params, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 0.0,
                  *, subgroup_size: int = 100_000_000, profile=None, stride="auto", static_ratio=0.0,
                  master_params=None, process_group=None, average_grads: bool = False, explore: int = 3,
-                 fused_gather: bool = True, fused_reduce: bool = True) -> None:
+                 fused_gather: bool = True, fused_reduce: bool = True, hbm_budget_bytes: int | None = None) -> None:
+        """``static_ratio``: the TwinFlow fraction of subgroups whose fp32
+        state is homed in HBM, or "auto" for as many as fit in
+        ``hbm_budget_bytes`` (default: the HBM free now minus a 4 GB headroom —
+        pass an explicit budget to leave room for activations)."""
         import torch
         import torch.distributed as dist
 
@@ -87,7 +91,8 @@ class DeepOptimizerStates:
         if static_ratio == "auto":
             # capacity-aware: as many subgroups homed in HBM as fit beside two
             # windows (the grads and working copy already live in the flat buffers)
-            r = policy.capacity_static_ratio(sizes, torch.cuda.mem_get_info(dev)[0], lowp_bytes_per_param=0)
+            budget = torch.cuda.mem_get_info(dev)[0] if hbm_budget_bytes is None else int(hbm_budget_bytes) + (4 << 30)
+            r = policy.capacity_static_ratio(sizes, budget, lowp_bytes_per_param=0)
             static_ratio = -self._max_over_ranks(-r) if self.world > 1 else r  # same plan shape everywhere
         static = build_plan(len(sizes), 1, static_ratio=static_ratio).static_set
         # sparse pinned pool: host memory only for the host-homed subgroups

@@ -18,6 +18,7 @@ to re-fit per iteration:
 
 from __future__ import annotations
 
+import ctypes
 import dataclasses
 import json
 import threading
@@ -201,6 +202,72 @@ def measure_h1(n: int = 100_000_000, with_dma: bool = False, reps: int = 3) -> d
     return out
 
 
+class _DuplexPump:
+    """Pinned duplex DMA in a background thread (64 MB per direction per
+    round); ``moved`` counts the host bytes the copy engines read + wrote."""
+
+    def __init__(self, nb: int = 1 << 26) -> None:
+        torch = _torch()
+        self.hx = torch.from_numpy(N.HostBuffer(nb).array(np.uint8, nb))
+        self.hy = torch.from_numpy(N.HostBuffer(nb).array(np.uint8, nb))
+        self.dx = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        self.dy = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        self.s1, self.s2 = torch.cuda.Stream(), torch.cuda.Stream()
+        self.nb, self.moved = nb, 0
+        self.stop = threading.Event()
+        self.th = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self) -> None:
+        torch = _torch()
+        while not self.stop.is_set():
+            with torch.cuda.stream(self.s1):
+                self.dx.copy_(self.hx, non_blocking=True)
+            with torch.cuda.stream(self.s2):
+                self.hy.copy_(self.dy, non_blocking=True)
+            self.s1.synchronize()
+            self.s2.synchronize()
+            self.moved += 2 * self.nb
+
+    def __enter__(self):
+        self.th.start()
+        time.sleep(0.05)
+        return self
+
+    def __exit__(self, *exc):
+        self.stop.set()
+        self.th.join()
+
+
+def measure_host_dram(nbytes: int = 1 << 31, reps: int = 3, with_dma: bool = True) -> dict:
+    """Host DRAM throughput of the whole team: a read pass and a copy pass
+    (memcpy, non-temporal stores), alone and with duplex pinned DMA running
+    (bytes the copy engines move count too).  ``peak_GBs`` — the best of
+    these — is the host-DRAM roofline's denominator."""
+    src = N.HostBuffer(nbytes)
+    dst = N.HostBuffer(nbytes)
+    lib = N.lib()
+    secs = ctypes.c_double()
+    out: dict = {}
+
+    def one(mode: int) -> tuple[float, int]:
+        N.check(lib.dos_host_membw(src.address, dst.address, nbytes, mode, 0, ctypes.byref(secs)))
+        return secs.value, nbytes * (1 if mode == 0 else 2)
+
+    for mode, name in ((0, "read"), (1, "copy")):
+        one(mode)
+        out[f"{name}_GBs"] = max(b / t for t, b in (one(mode) for _ in range(reps))) / 1e9
+        if with_dma:
+            with _DuplexPump() as pump:
+                t0, m0, cpu = time.perf_counter(), pump.moved, 0
+                for _ in range(reps):
+                    cpu += one(mode)[1]
+                dt, dma = time.perf_counter() - t0, pump.moved - m0
+            out[f"{name}_with_dma_GBs_combined"] = (cpu + dma) / dt / 1e9
+            out[f"{name}_with_dma_dma_GBs"] = dma / dt / 1e9
+    out["peak_GBs"] = max(v for k, v in out.items() if k.endswith("_GBs") or k.endswith("_combined"))
+    return out
+
+
 def measure_profile(fast_capacity_bytes: int | None = None, save: bool = False, quick: bool = False) -> SystemProfile:
     """Measure all planner constants on this box; returns a SystemProfile."""
     n = 25_000_000 if quick else 100_000_000
@@ -226,8 +293,10 @@ def measure_profile(fast_capacity_bytes: int | None = None, save: bool = False, 
         caveat="measured by profile_b200.measure_profile",
     )
     link_h1 = measure_link_under_h1(1 << 28)
+    dram = measure_host_dram(1 << 30 if quick else 1 << 31)
     LAST_RAW.clear()
     LAST_RAW.update({"link": link, "k1": k1, "h1_alone": h1_alone, "h1_with_dma": h1_busy, "link_under_h1": link_h1,
+                     "host_dram": dram,
                      "link_slowdown_under_h1": max(1.0, link["duplex_GBs_per_dir"] / link_h1["duplex_GBs_per_dir"])})
     if save:
         d = dataclasses.asdict(prof)

@@ -65,3 +65,15 @@ def test_capacity_aware_state_dict_roundtrip():
     sd2 = opt.state_dict()
     for k in ("params32", "momentum32", "variance32"):
         assert sd2[k].tobytes() == sd[k].tobytes()
+
+
+def test_capacity_aware_respects_hbm_budget():
+    model = _model()
+    n = sum(p.numel() for p in model.parameters())
+    # room for two windows of 20k params and two residents: the rest stays on the host
+    budget = 2 * 12 * 20_000 + 2 * 12 * 20_000
+    opt = DeepOptimizerStates(model.parameters(), subgroup_size=20_000, profile=get_profile("h100-node"),
+                              stride=2, static_ratio="auto", hbm_budget_bytes=budget)
+    nsg = -(-n // 20_000)
+    assert opt.static_ratio == 2 / nsg and len(opt.plan.static_set) == 2
+    assert 0 < opt.opt.host_bytes
