@@ -72,6 +72,8 @@ struct Engine {
   std::vector<cudaEvent_t> ev_g;                      // per action: its grads are on the host
   std::vector<cudaEvent_t> ev_sg;                     // per subgroup: host_io grads of a static resident landed
   std::deque<int32_t> static_q;                       // host_io_ahead: resident updates whose grads are in flight
+  static constexpr int kFlushAhead = 2;               // flush_grads: host updates a grad flush may run ahead
+  std::deque<int32_t> flush_q;                        // flush_grads: host updates whose grads were flushed
   int nslots = 0;
   int64_t slot_elems = 0;
   float* slot_mem = nullptr;
@@ -257,6 +259,19 @@ struct Engine {
         // §8(f) row 1 inside the phase: this subgroup's half-precision grads
         // D2H on their own stream, in emission (= subgroup) order
         const int64_t start = sg_start[sg], n = sg_size[sg];
+        // Throttle: this subgroup's flush is issued once the host lane has
+        // finished the CPU update kFlushAhead positions earlier, so the grads
+        // still land well before H1 needs them but the D2H copy engine is not
+        // monopolised by every host subgroup's grads at phase start (the
+        // streamed windows' FLUSH_OUT_* share it).
+        if ((int)flush_q.size() >= kFlushAhead) {
+          const int32_t d = flush_q.front();
+          flush_q.pop_front();
+          if (wait_value_ok && wait_fn &&
+              wait_fn((CUstream)gst, flags_dev + 4 * (CUdeviceptr)d, epoch, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+            wait_value_ok = false;
+        }
+        flush_q.push_back(a->id);
         if (gsrc.n > 0) {  // fused reduce-scatter of this subgroup, in place in dev_g, then the flush
           const int rc = dos_reduce_launch(static_cast<char*>(const_cast<void*>(S.dev_g)) + 2 * start, S.lowp_dtype, n,
                                            dos_gsrc_offset(gsrc, start), gst);
@@ -495,6 +510,7 @@ struct Engine {
     DOS_CU(cudaStreamWaitEvent(st[2], ev0, 0));
     DOS_CU(cudaStreamWaitEvent(gst, ev0, 0));
     DOS_CU(cudaStreamWaitEvent(ost, ev0, 0));
+    flush_q.clear();
     if (S.host_io) {
       // static residents' grads go H2D first thing, on the side stream, so
       // their updates (STATIC_LAST: at the end of the phase) never wait on them
