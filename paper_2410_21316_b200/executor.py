@@ -159,6 +159,16 @@ class ExecutionResult:
     measured: Timeline | None = None  # wall-clock timeline of the B200 run
 
 
+def _under_profiler() -> bool:
+    """Nsight Compute (ncu) injects itself through CUDA_INJECTION64_PATH and
+    replays each kernel: CUDA-event timestamps around a replayed kernel are
+    not a timeline, so the measured-timeline audit is skipped under it (the
+    numeric results are unaffected; ncu runs are never timing runs)."""
+    import os
+
+    return bool(os.environ.get("CUDA_INJECTION64_PATH")) or any(k.startswith("NV_NSIGHT") for k in os.environ)
+
+
 def execute_plan(
     optimizer: ShardedOptimizer,
     plan: UpdatePlan,
@@ -223,7 +233,7 @@ def execute_plan(
     target.residency.after_phase(host_io)
     sizes = target.sizes
     measured = build_timeline(plan, measured_events, sizes) if measured_events else None
-    if validate_measured and measured_events:
+    if validate_measured and measured_events and not _under_profiler():
         validate_schedule(plan, measured_events, target, check_streams=False, max_windows=target.num_slots,
                           tolerance_ns=MEASURED_CLOCK_SLACK_NS)
     optimizer.step = step
