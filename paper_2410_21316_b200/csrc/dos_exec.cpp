@@ -72,7 +72,7 @@ struct Engine {
   std::vector<cudaEvent_t> ev_g;                      // per action: its grads are on the host
   std::vector<cudaEvent_t> ev_sg;                     // per subgroup: host_io grads of a static resident landed
   std::deque<int32_t> static_q;                       // host_io_ahead: resident updates whose grads are in flight
-  static constexpr int kFlushAhead = 2;               // flush_grads: host updates a grad flush may run ahead
+  static constexpr int kFlushAhead = 4;               // flush_grads: host updates a grad flush may run ahead
   std::deque<int32_t> flush_q;                        // flush_grads: host updates whose grads were flushed
   int nslots = 0;
   int64_t slot_elems = 0;
