@@ -145,6 +145,12 @@ class DeviceResidency:
                     self._d2h(getattr(opt, name)[a:a + n], self.static_sg[sg][k])
 
     def sync_all_host(self) -> None:
+        """Make every host image current (a host-side pass over the whole
+        shard follows).  In a sparse pool every range is committed first:
+        an uncommitted static resident's range is filled from its HBM home."""
+        n = len(self.opt.subgroups)
+        self.opt.ensure_host(range(n), "state")
+        self.opt.ensure_host(range(n), "lowp")
         for name in ("_w", "_p", "_m", "_v"):
             self.sync_host(name)
 

@@ -96,3 +96,17 @@ def test_sparse_host_io_commits_grads_and_matches(h100, placement):
     D.execute_plan(opt, plan, h100, HYPER, host_io=True)
     O.sequential_oracle(want)
     assert_matches(opt, want)
+
+
+def test_host_side_oracle_on_a_sparse_shard(h100):
+    """A host-side pass (sequential_oracle / adam_step_subgroup) over a shard
+    whose residents live only in HBM first pulls them to the host, so the
+    host update sees their real state and the re-upload keeps it."""
+    total, sg = 6 * (1 << 20), 1 << 20
+    plan = D.build_plan(6, 2, static_ratio=0.5, placement=Placement.STATIC_FIRST)
+    opt, want = sparse_shard(total, sg, 4, "bf16", plan.static_set)
+    D.sequential_oracle(opt, HYPER)
+    O.sequential_oracle(want)
+    D.execute_plan(opt, plan, h100, HYPER)  # the residents' HBM homes were refreshed from the host pass
+    O.sequential_oracle(want)
+    assert_matches(opt, want)
