@@ -262,6 +262,10 @@ class B200Bench:
             from paper_2410_21316_b200.distributed import bind_host_cores
 
             self.cores = bind_host_cores(local, int(os.environ.get("LOCAL_WORLD_SIZE", world)))
+        # the pinned pool on the GPU's NUMA node (first touch by the rank's own team otherwise)
+        from paper_2410_21316_b200.distributed import gpu_numa_node
+
+        self.numa = gpu_numa_node(dev_index) if world > 1 else -1
         if args.host_threads > 0:
             D._native.lib().dos_set_host_threads(args.host_threads)
         self.P, self.SG = int(args.params), int(args.subgroup)
@@ -333,7 +337,7 @@ class B200Bench:
         static = D.build_plan(self.nsg, 1, static_ratio=self.static_ratio, placement=self.placement).static_set
         t0 = time.perf_counter()
         # sparse pinned pool: host memory only for the host-homed subgroups
-        self.opt = D.ShardedOptimizer.allocate(self.P_rank, self.SG, lowp=a.lowp,
+        self.opt = D.ShardedOptimizer.allocate(self.P_rank, self.SG, lowp=a.lowp, numa_node=self.numa,
                                                host_homed=[i for i in range(self.nsg) if i not in static])
         t1 = time.perf_counter()
         res = self.opt.to_device(self.device)

@@ -349,6 +349,19 @@ def _parse_cpulist(text: str) -> list[int]:
     return out
 
 
+def gpu_numa_node(device_index: int) -> int:
+    """NUMA node of a GPU from sysfs (-1 when unknown)."""
+    import torch
+
+    try:
+        p = torch.cuda.get_device_properties(device_index)
+        bus = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bus}/numa_node") as fh:
+            return int(fh.read().strip())
+    except Exception:
+        return -1
+
+
 def bind_host_cores(local_rank: int, local_world: int) -> list[int]:
     """Restrict this process (and libdos's H1 team) to its share of the host
     cores: the CPUs of its GPU's NUMA node, split among the local ranks on
@@ -359,16 +372,8 @@ def bind_host_cores(local_rank: int, local_world: int) -> list[int]:
 
     from . import _native as N
 
-    def gpu_node(i: int) -> int:
-        try:
-            p = torch.cuda.get_device_properties(i)
-            bus = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
-            with open(f"/sys/bus/pci/devices/{bus}/numa_node") as fh:
-                return int(fh.read().strip())
-        except Exception:
-            return -1
-
-    nodes = [gpu_node(i) for i in range(local_world)] if torch.cuda.device_count() >= local_world else [-1] * local_world
+    nodes = ([gpu_numa_node(i) for i in range(local_world)] if torch.cuda.device_count() >= local_world
+             else [-1] * local_world)
     node_cpus: dict[int, list[int]] = {}
     for nd in set(nodes):
         if nd >= 0:
