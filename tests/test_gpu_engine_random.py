@@ -1,7 +1,8 @@
 """Randomised engine options, bit-exact against the oracle on the B200:
 stride, static ratio/placement, one or two HBM windows, host_io,
 in-phase grad flush, fused/unfused downscale, fp16/bf16, ragged sizes,
-two consecutive steps with re-planning in between."""
+dense or sparse pinned pool, two consecutive steps with re-planning in
+between."""
 from __future__ import annotations
 
 import dataclasses
@@ -34,18 +35,51 @@ def _instance(rng):
     return total, sg, lowp, hyper, steps
 
 
+def _plan(n, s):
+    if s["ratio"] * n >= n - 1e-9 and s["stride"] is not D.ALL_CPU:
+        return D.build_plan(n, s["stride"])
+    return D.build_plan(n, s["stride"], s["ratio"], s["placement"])
+
+
+def _t(a):
+    return torch.from_numpy(a.view(np.int16) if a.itemsize == 2 else a)
+
+
+def _sparse(total, sg, seed, lowp, static):
+    """The oracle's shard in a sparse pool: host memory only for the first
+    plan's host-homed subgroups, residents written straight into HBM."""
+    ref = O.initialize(total, sg, seed, lowp)
+    n = -(-total // sg)
+    opt = D.ShardedOptimizer.allocate(total, sg, lowp=lowp, host_homed=[i for i in range(n) if i not in static])
+    for a, b in opt.host_runs("state"):
+        opt._p[a:b], opt._m[a:b], opt._v[a:b] = ref["p"][a:b], ref["m"][a:b], ref["v"][a:b]
+    for a, b in opt.host_runs("lowp"):
+        opt._g[a:b], opt._w[a:b] = ref["g"][a:b], ref["w"][a:b]
+    res = opt.to_device()
+    res.set_static(static)
+    for i in static:
+        g = opt.subgroups[i]
+        for t, key in zip(res.static_views(i), "pmv"):
+            t.copy_(_t(ref[key][g.slice]))
+        res.grads.view(torch.int16)[g.slice].copy_(_t(ref["g"][g.slice]))
+        res.model16.view(torch.int16)[g.slice].copy_(_t(ref["w"][g.slice]))
+    return opt
+
+
 def test_random_engine_options_match_oracle(h100):
     rng = np.random.default_rng(20261017)
-    for case in range(40):
+    for case in range(48):
         total, sg, lowp, hyper, steps = _instance(rng)
         seed = int(rng.integers(0, 2**31))
-        opt = D.ShardedOptimizer.initialize(total, sg, seed=seed, lowp=lowp)
-        opt.to_device()
+        n = -(-total // sg)
+        if rng.integers(0, 3) == 0:  # a third of the cases in a sparse pinned pool
+            opt = _sparse(total, sg, seed, lowp, _plan(n, steps[0]).static_set)
+        else:
+            opt = D.ShardedOptimizer.initialize(total, sg, seed=seed, lowp=lowp)
+            opt.to_device()
         ref = O.initialize(total, sg, seed, lowp)
         for s in steps:
-            n = len(opt.subgroups)
-            plan = D.build_plan(n, s["stride"], s["ratio"], s["placement"]) if not (
-                s["ratio"] * n >= n - 1e-9 and s["stride"] is not D.ALL_CPU) else D.build_plan(n, s["stride"])
+            plan = _plan(n, s)
             cap = s["windows"] * 12 * sg
             prof = dataclasses.replace(h100, fast_capacity_bytes=cap)
             D.execute_plan(opt, plan, prof, D.AdamHyper(**hyper), host_io=s["mode"] == "host_io",
