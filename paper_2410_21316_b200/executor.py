@@ -282,7 +282,6 @@ def flush_gradients(optimizer: ShardedOptimizer, profile: SystemProfile, strateg
     P = optimizer.total_params
     elems = chunk_bytes // 2
     res = optimizer.residency
-    g = optimizer.grads16
     if res is not None and strategy is GradFlushStrategy.GPU_UPSCALE_FP32:
         # chunk-wise on-device upcast double-buffered against
         # the pinned fp32 D2H: chunk k+1 converts while chunk k crosses the link
@@ -311,6 +310,7 @@ def flush_gradients(optimizer: ShardedOptimizer, profile: SystemProfile, strateg
                 done[k % 2].record(copy)
         copy.synchronize()
     else:
+        g = optimizer.grads16
         out = np.empty(P, dtype=np.float32)
         for lo in range(0, P, elems):
             hi = min(lo + elems, P)
