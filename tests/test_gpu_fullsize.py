@@ -1,6 +1,8 @@
 """Parity at BASELINE's full sizes on the B200: a 7B shard (configs[1], 20%
-HBM-resident, stride 5) and a 13B shard (configs[2], capacity-aware
-residency, sparse host pool) run real update phases; sampled subgroups —
+HBM-resident, stride 5), a 13B shard (configs[2], capacity-aware
+residency, sparse host pool) and one rank of 70B/8 (configs[4]: 8.75e9
+params, 88 subgroups with a ragged 5e7 tail, 50% resident) run real update
+phases; sampled subgroups —
 first, last, and one of each kind (static resident, host-updated, streamed
 through the GPU) — are snapshotted before the second step and checked bit for
 bit against the C oracle (oracle/adam_oracle.c, pinned to the reference) on
@@ -24,7 +26,7 @@ def _bits(t) -> np.ndarray:
     return t.detach().view(torch.int32 if t.element_size() == 4 else torch.int16).cpu().numpy().copy()
 
 
-@pytest.mark.parametrize("params, ratio, stride", [(7e9, 0.2, 5), (13e9, "auto", 6)])
+@pytest.mark.parametrize("params, ratio, stride", [(7e9, 0.2, 5), (13e9, "auto", 6), (8.75e9, 0.5, 3)])
 def test_full_size_sampled_parity(params, ratio, stride):
     from bench import fill_shard, host_available_bytes
     from oracle import c_oracle
