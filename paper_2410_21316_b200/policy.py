@@ -169,7 +169,7 @@ class StrideTuner:
     def __init__(self, profile: SystemProfile, sizes: Sequence[int], candidates: Iterable = range(1, 7),
                  static_ratio: float = 0.0, explore: int = 4, num_slots: int = 2,
                  link_slowdown: float = 1.0, hill_climb: bool = True,
-                 placement: Placement = Placement.STATIC_LAST) -> None:
+                 placement: Placement = Placement.STATIC_LAST, refine: bool = True) -> None:
         self.sizes = list(sizes)
         self.static_ratio = static_ratio
         self.placement = placement
@@ -179,6 +179,7 @@ class StrideTuner:
         self.predicted = spans
         self.measured: dict = {}
         self.hill_climb = hill_climb
+        self.refine = refine
 
     def next_stride(self):
         if self.queue:
@@ -194,6 +195,11 @@ class StrideTuner:
             if best is not ALL_CPU:
                 top = max(1, len(self.sizes))
                 self.queue = [k for k in (best + 1, best - 1) if 1 <= k <= top and k not in self.measured][:1]
+        if not self.queue and self.refine and len(self.measured) > 1:
+            # one more sample of the two fastest (spans are kept as the min
+            # over samples), so a single noisy step does not pick the stride
+            self.refine = False
+            self.queue = sorted(self.measured, key=lambda k: self.measured[k])[:2]
 
     @property
     def exploring(self) -> bool:

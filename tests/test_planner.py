@@ -321,7 +321,7 @@ def test_b200_model_timelines_validate_without_stream_fifo(h100):
 def test_stride_tuner_explores_then_exploits(h100):
     from paper_2410_21316_b200 import policy
 
-    tuner = policy.StrideTuner(h100, [10**8] * 20, range(1, 7), explore=3, hill_climb=False)
+    tuner = policy.StrideTuner(h100, [10**8] * 20, range(1, 7), explore=3, hill_climb=False, refine=False)
     tried = []
     fake = {1: 900, 2: 500, 3: 400, 4: 450, 5: 700, 6: 800}
     while tuner.exploring:
@@ -341,7 +341,7 @@ def test_stride_tuner_hill_climbs_past_the_predicted_set(h100, optimum):
     from paper_2410_21316_b200 import policy
 
     n = 20
-    tuner = policy.StrideTuner(h100, [10**8] * n, range(1, 7), explore=3)
+    tuner = policy.StrideTuner(h100, [10**8] * n, range(1, 7), explore=3, refine=False)
     fake = lambda k: 1000 + 37 * abs(k - optimum)  # unimodal in the stride
     tried = []
     while tuner.exploring:
@@ -352,6 +352,25 @@ def test_stride_tuner_hill_climbs_past_the_predicted_set(h100, optimum):
         assert len(tried) <= n
     assert tuner.next_stride() == optimum
     assert all(k in tuner.measured for k in (optimum - 1, optimum + 1) if 1 <= k <= n)
+
+
+def test_stride_tuner_refines_the_two_fastest(h100):
+    """After exploring, the two fastest strides get one more sample; spans
+    keep the minimum, so one step slowed by noise does not decide."""
+    from paper_2410_21316_b200 import policy
+
+    tuner = policy.StrideTuner(h100, [10**8] * 20, range(1, 7), explore=3, hill_climb=False)
+    first = {}
+    samples = {1: [900, 900], 2: [560, 500], 3: [520, 520], 4: [600, 600], 5: [700, 700], 6: [800, 800]}
+    tried = []
+    while tuner.exploring:
+        k = tuner.next_stride()
+        tried.append(k)
+        tuner.record(k, samples[k][first.setdefault(k, 0)])
+        first[k] += 1
+    assert len(tried) == len(set(tried)) + 2  # the two fastest measured twice
+    best = min(set(tried), key=lambda k: min(samples[k]))
+    assert tuner.next_stride() == best
 
 
 def test_refit_profile_from_a_timeline(h100):
