@@ -221,17 +221,20 @@ def execute_plan(
     target = B200Target(profile, plan, optimizer, hyper, step, host_threads=host_threads, host_io=host_io,
                         peers=peers, flush_grads=flush_grads, fuse_downscale=fuse_downscale,
                         grad_sources=grad_sources)
+    sizes = target.sizes
     try:
         events = run_update(plan, target)
         if on_submitted is not None:  # e.g. chain per-subgroup collectives onto engine events
             on_submitted(target)
+        # the predicted timeline's audit and summary need no device results:
+        # done while the phase runs
+        validate_schedule(plan, events, target)
+        timeline = build_timeline(plan, events, sizes)
     except BaseException:
         target.finish(raise_errors=False)
         raise
     measured_events = target.finish()
-    validate_schedule(plan, events, target)
     target.residency.after_phase(host_io)
-    sizes = target.sizes
     measured = build_timeline(plan, measured_events, sizes) if measured_events else None
     if validate_measured and measured_events and not _under_profiler():
         validate_schedule(plan, measured_events, target, check_streams=False, max_windows=target.num_slots,
@@ -243,7 +246,6 @@ def execute_plan(
         for sg in optimizer.subgroups:
             if want[sg.slice].tobytes() != w[sg.slice].tobytes():
                 raise AssertionError(f"model16 of subgroup {sg.index} incoherent with params32")
-    timeline = build_timeline(plan, events, sizes)
     if mode is ExecMode.THROTTLED:
         _pace_replay(timeline, throttle_scale)
     return ExecutionResult(optimizer=optimizer, timeline=timeline, step=step, mode=mode, measured=measured)
