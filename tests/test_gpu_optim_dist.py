@@ -23,7 +23,7 @@ def _port() -> int:
     return p
 
 
-def _worker(rank, world, port, stride, fused, q, fused_reduce=False, average=False):
+def _worker(rank, world, port, stride, fused, q, fused_reduce=False, average=False, static_ratio=0.2):
     try:
         import torch.distributed as dist
 
@@ -39,7 +39,7 @@ def _worker(rank, world, port, stride, fused, q, fused_reduce=False, average=Fal
             torch.bfloat16)
         init = torch.cat([p.detach().reshape(-1) for p in model.parameters()]).float().cpu().numpy().copy()
         opt = DeepOptimizerStates(model.parameters(), lr=1e-3, subgroup_size=9_000, profile=get_profile("h100-node"),
-                                  stride=stride, static_ratio=0.2, process_group=dist.group.WORLD,
+                                  stride=stride, static_ratio=static_ratio, process_group=dist.group.WORLD,
                                   fused_gather=fused, fused_reduce=fused_reduce, average_grads=average)
         lay, off = opt.layout, opt.offset
         mine = opt.opt.total_params
@@ -69,10 +69,11 @@ def _worker(rank, world, port, stride, fused, q, fused_reduce=False, average=Fal
         q.put((rank, False, traceback.format_exc()))
 
 
-@pytest.mark.parametrize("stride,fused,fused_reduce,average", [
-    (2, False, False, False), ("auto", False, False, False), (2, True, False, False), ("auto", True, False, True),
-    (2, True, True, False), ("auto", True, True, True), (3, False, True, False)])
-def test_two_rank_zero3_step_matches_oracle(stride, fused, fused_reduce, average):
+@pytest.mark.parametrize("stride,fused,fused_reduce,average,static_ratio", [
+    (2, False, False, False, 0.2), ("auto", False, False, False, 0.2), (2, True, False, False, 0.2),
+    ("auto", True, False, True, 0.2), (2, True, True, False, 0.2), ("auto", True, True, True, 0.2),
+    (3, False, True, False, 0.2), (2, True, True, False, "auto")])
+def test_two_rank_zero3_step_matches_oracle(stride, fused, fused_reduce, average, static_ratio):
     """fused: all-gather in K1's epilogue; fused_reduce: reduce-scatter in
     K1's grad load (both over CUDA IPC); otherwise the bucketed collectives."""
     import torch.multiprocessing as mp
@@ -80,7 +81,7 @@ def test_two_rank_zero3_step_matches_oracle(stride, fused, fused_reduce, average
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, stride, fused, q, fused_reduce, average))
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, stride, fused, q, fused_reduce, average, static_ratio))
              for r in range(2)]
     for p in procs:
         p.start()
