@@ -210,11 +210,15 @@ class DeviceResidency:
         leaving = sorted(self.static_set - static_set)
         joining = sorted(static_set - self.static_set)
         if leaving:
+            # ranges committed just now are filled from HBM by on_host_commit;
+            # the others get their (possibly newer) HBM state written home here
+            had_home = [sg for sg in leaving if opt.host_committed(sg, "state")]
             opt.ensure_host(leaving, "state")
-            for sg in leaving:
+            for sg in had_home:
                 a, n = int(self.sg_start[sg]), int(self.sg_size[sg])
                 for k, name in enumerate(("_p", "_m", "_v")):
                     self._d2h(getattr(opt, name)[a:a + n], self.static_sg[sg][k])
+            for sg in leaving:
                 del self.static_sg[sg]
                 self.static_off[sg] = -1
                 for k in range(3):
