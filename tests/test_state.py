@@ -222,3 +222,21 @@ def test_sparse_pool_abi_errors():
         hb.commit(1 << 22, 1)
     with pytest.raises(ValueError):
         N.check(N.lib().dos_host_commit(12345, 0, 1))
+
+
+def test_host_membw_probe():
+    import ctypes
+
+    from paper_2410_21316_b200 import _native as N
+
+    a, b = N.HostBuffer(1 << 22, register_cuda=False), N.HostBuffer(1 << 22, register_cuda=False)
+    secs = ctypes.c_double()
+    for mode in (0, 1):
+        N.check(N.lib().dos_host_membw(a.address, b.address, 1 << 22, mode, 0, ctypes.byref(secs)))
+        assert secs.value > 0
+    a.array(np.uint8, 1 << 22)[:] = 7
+    N.check(N.lib().dos_host_membw(a.address, b.address, 1 << 22, 1, 0, ctypes.byref(secs)))
+    assert (b.array(np.uint8, 1 << 22) == 7).all()  # the copy pass really copies
+    for bad in ((a.address, b.address, 1 << 22, 2), (a.address, None, 1 << 22, 1), (None, b.address, 64, 0)):
+        with pytest.raises(ValueError):
+            N.check(N.lib().dos_host_membw(*bad, 0, ctypes.byref(secs)))
