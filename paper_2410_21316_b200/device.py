@@ -188,6 +188,42 @@ class DeviceResidency:
             else:
                 dst.zero_()
 
+    # ---- whole-shard export / import without materialising a sparse pool
+    def export_state(self, name: str) -> np.ndarray:
+        """A fresh (pageable) copy of ``params32``/``momentum32``/``variance32``
+        ("_p"/"_m"/"_v") assembled from each subgroup's home tier — the host
+        pool for host-homed subgroups, HBM for static residents — without
+        committing any host range (a checkpoint of a shard larger than the
+        host pool stays possible)."""
+        k = ("_p", "_m", "_v").index(name)
+        opt = self.opt
+        src = getattr(opt, name)
+        out = np.empty(opt.total_params, dtype=np.float32)
+        for sg in opt.subgroups:
+            if sg.index in self.static_set:
+                out[sg.slice] = self.static_sg[sg.index][k].cpu().numpy()
+            else:
+                out[sg.slice] = src[sg.slice]
+        return out
+
+    def import_state(self, name: str, values: np.ndarray) -> None:
+        """Inverse of ``export_state``: each subgroup's slice goes to its home."""
+        torch = _torch()
+        k = ("_p", "_m", "_v").index(name)
+        opt = self.opt
+        values = np.ascontiguousarray(values, dtype=np.float32).reshape(-1)
+        if values.size != opt.total_params:
+            raise ValueError(f"{name} must hold {opt.total_params} elements")
+        opt.ensure_host([g.index for g in opt.subgroups if g.index not in self.static_set], "state")
+        dst = getattr(opt, name)
+        for sg in opt.subgroups:
+            if sg.index in self.static_set:
+                self.static_sg[sg.index][k].copy_(torch.from_numpy(values[sg.slice]))
+            else:
+                dst[sg.slice] = values[sg.slice]
+        if self.static_set:  # residents' host images (where committed) are now behind HBM
+            self.host_stale.add(name)
+
     def static_views(self, sg: int) -> tuple:
         """(p, m, v) fp32 HBM tensors of static subgroup ``sg`` (its home
         while resident: write them to initialise a device-homed subgroup)."""

@@ -88,13 +88,16 @@ class DeepOptimizerStates:
                 off += n
 
         sizes = [g.size for g in lay.ranks[self.rank]]
+        # "auto" may resolve to every subgroup resident on purpose: plan without the all-static warning
+        self._plan = policy._quiet_plan if static_ratio == "auto" else (
+            lambda n, k, r: build_plan(n, k, static_ratio=r))
         if static_ratio == "auto":
             # capacity-aware: as many subgroups homed in HBM as fit beside two
             # windows (the grads and working copy already live in the flat buffers)
             budget = torch.cuda.mem_get_info(dev)[0] if hbm_budget_bytes is None else int(hbm_budget_bytes) + (4 << 30)
             r = policy.capacity_static_ratio(sizes, budget, lowp_bytes_per_param=0)
             static_ratio = -self._max_over_ranks(-r) if self.world > 1 else r  # same plan shape everywhere
-        static = build_plan(len(sizes), 1, static_ratio=static_ratio).static_set
+        static = self._plan(len(sizes), 1, static_ratio).static_set
         # sparse pinned pool: host memory only for the host-homed subgroups
         opt = ShardedOptimizer.allocate(mine, sg, lowp=self.lowp,
                                         host_homed=[i for i in range(len(sizes)) if i not in static])
@@ -146,7 +149,7 @@ class DeepOptimizerStates:
                 dist.broadcast_object_list(box, src=0, group=process_group)
                 self.tuner.queue = list(box[0])
             stride = self.tuner.next_stride()
-        self.plan = build_plan(len(self.sizes), stride, static_ratio=static_ratio)
+        self.plan = self._plan(len(self.sizes), stride, static_ratio)
         self.last = None
 
     @property
@@ -222,7 +225,7 @@ class DeepOptimizerStates:
             self.tuner.record(self.plan.stride, int(self._max_over_ranks(self.last.measured.span_ns)))
             nxt = self.tuner.next_stride()
             if nxt != self.plan.stride:
-                self.plan = build_plan(len(self.sizes), nxt, static_ratio=self.static_ratio)
+                self.plan = self._plan(len(self.sizes), nxt, self.static_ratio)
         return self.last
 
     def master_params(self) -> np.ndarray:
@@ -230,20 +233,26 @@ class DeepOptimizerStates:
         return self.opt.params32
 
     def state_dict(self) -> dict:
+        """This rank's fp32 state, each subgroup read from its home tier (a
+        sparse pool is not materialised on the host)."""
+        res = self.res
         return {"step": self.opt.step, "rank": self.rank, "world": self.world, "offset": self.offset,
-                "params32": self.opt.params32.copy(), "momentum32": self.opt.momentum32.copy(),
-                "variance32": self.opt.variance32.copy(), "hyper": self.hyper}
+                "params32": res.export_state("_p"), "momentum32": res.export_state("_m"),
+                "variance32": res.export_state("_v"), "hyper": self.hyper}
 
     def load_state_dict(self, sd: dict) -> None:
+        import torch
+
         if (sd.get("rank", 0), sd.get("world", 1)) != (self.rank, self.world):
             raise ValueError("state dict belongs to another rank / world size")
-        n = len(self.opt.subgroups)
-        self.opt.ensure_host(range(n), "state")  # a sparse pool: every range gets a host image
-        self.opt.ensure_host(range(n), "lowp")
-        self.res.sync_all_host()
-        self.opt._p[:] = sd["params32"]
-        self.opt._m[:] = sd["momentum32"]
-        self.opt._v[:] = sd["variance32"]
-        self.opt.step = int(sd["step"])
-        self.opt._w[:] = lowp_downscale(self.opt._p, self.lowp)
-        self.res.push_host()
+        res, opt = self.res, self.opt
+        for name, key in (("_p", "params32"), ("_m", "momentum32"), ("_v", "variance32")):
+            res.import_state(name, sd[key])
+        opt.step = int(sd["step"])
+        # the working copy (this rank's chunk of the model) = RNE of the masters
+        w = lowp_downscale(np.ascontiguousarray(sd["params32"], dtype=np.float32), self.lowp)
+        with torch.no_grad():
+            res.model16.view(torch.int16).copy_(torch.from_numpy(w.view(np.int16)))
+        for a, b in opt.host_runs("lowp"):
+            opt._w[a:b] = w[a:b]
+        res.host_stale.discard("_w")

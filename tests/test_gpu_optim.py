@@ -58,8 +58,10 @@ def test_capacity_aware_state_dict_roundtrip():
         model(x).float().pow(2).mean().backward()
         opt.step()
     sd = opt.state_dict()
+    assert opt.opt.host_bytes == 0  # exported from HBM without materialising the sparse pool
     before = torch.cat([p.detach().reshape(-1) for p in model.parameters()]).clone()
     opt.load_state_dict(sd)
+    assert opt.opt.host_bytes == 0
     after = torch.cat([p.detach().reshape(-1) for p in model.parameters()])
     assert torch.equal(before.view(torch.int16), after.view(torch.int16))
     sd2 = opt.state_dict()
@@ -77,3 +79,31 @@ def test_capacity_aware_respects_hbm_budget():
     nsg = -(-n // 20_000)
     assert opt.static_ratio == 2 / nsg and len(opt.plan.static_set) == 2
     assert 0 < opt.opt.host_bytes
+
+
+@pytest.mark.parametrize("static_ratio", [0.0, 0.5])
+def test_state_dict_roundtrip_continues_training_exactly(static_ratio):
+    """Save after two steps, perturb, load, take a step: identical to taking
+    that step straight after the save."""
+    def run(load_from=None):
+        model = _model()
+        opt = DeepOptimizerStates(model.parameters(), subgroup_size=20_000, profile=get_profile("h100-node"),
+                                  stride=2, static_ratio=static_ratio)
+        x = torch.randn(32, 256, device="cuda", dtype=torch.bfloat16, generator=torch.Generator("cuda").manual_seed(3))
+        for _ in range(2):
+            opt.zero_grad()
+            model(x).float().pow(2).mean().backward()
+            opt.step()
+        sd = opt.state_dict()
+        if load_from is not None:
+            opt.load_state_dict(load_from)
+        opt.zero_grad()
+        model(x).float().pow(2).mean().backward()
+        opt.step()
+        return sd, torch.cat([p.detach().reshape(-1) for p in model.parameters()]).clone(), opt.state_dict()
+
+    sd, params_a, end_a = run()
+    _, params_b, end_b = run(load_from=sd)
+    assert torch.equal(params_a.view(torch.int16), params_b.view(torch.int16))
+    for k in ("params32", "momentum32", "variance32"):
+        assert end_a[k].tobytes() == end_b[k].tobytes()
