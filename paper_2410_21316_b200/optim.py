@@ -229,8 +229,9 @@ class DeepOptimizerStates:
         return self.last
 
     def master_params(self) -> np.ndarray:
-        """This rank's fp32 master params (host image, synchronised)."""
-        return self.opt.params32
+        """This rank's fp32 master params (a copy assembled from each
+        subgroup's home tier; a sparse pool is not materialised)."""
+        return self.res.export_state("_p")
 
     def state_dict(self) -> dict:
         """This rank's fp32 state, each subgroup read from its home tier (a
