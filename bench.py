@@ -399,8 +399,9 @@ class B200Bench:
     def tune(self, ratio: float, explore: int):
         D = self.D
         slowdown = float(self.broadcast(self.profile_b200.LAST_RAW.get("link_slowdown_under_h1", 1.0)))
+        rates = self.broadcast(self.profile_b200.host_rates())  # the fluid host-DRAM model ranks the strides
         tuner = self.policy.StrideTuner(self.profile, self.sizes, range(1, 7), ratio, explore=explore,
-                                        link_slowdown=slowdown, placement=self.placement)
+                                        link_slowdown=slowdown, placement=self.placement, rates=rates)
         tuner.queue = list(self.broadcast(tuner.queue))  # same exploration order on every rank
         while tuner.exploring:
             k = tuner.next_stride()

@@ -10,6 +10,10 @@ previous iteration, and a split chosen per iteration.
 FIFO across directions (each in-flight window has its own HBM slot), and a
 window opens only when the window ``num_slots`` earlier has fully flushed.
 FLUSH_OUT_MODEL16 and CPU_DOWNSCALE cost nothing (fused into K1 / H1).
+``simulate_b200_fluid`` adds what the list scheduler cannot express: the
+host DRAM is shared by the host team and the copy engines, so their rates
+are fluid (scaled together whenever their joint host-memory traffic exceeds
+the measured peak); with measured ``HostRates`` it is the predictor.
 ``choose_stride`` takes the candidate with the smallest predicted span.
 """
 
@@ -128,14 +132,33 @@ def simulate_b200_phase(plan: UpdatePlan, profile: SystemProfile, subgroup_size:
     return build_timeline(plan, tuple(out), sizes)
 
 
+@dataclasses.dataclass(frozen=True)
+class HostRates:
+    """Measured rates for ``simulate_b200_fluid`` (bytes/s, params/s)."""
+
+    link_bytes_per_s: float       # pinned copy per direction, duplex
+    host_params_per_s: float      # H1 alone (uncontended)
+    fast_params_per_s: float      # K1
+    host_dram_bytes_per_s: float  # best measured host-memory throughput
+
+
 def choose_stride(profile: SystemProfile, sizes: Sequence[int], candidates: Iterable = range(1, 7),
-                  static_ratio: float = 0.0, num_slots: int = 2, link_slowdown: float = 1.0):
-    """Stride with the smallest predicted B200 span; returns (stride, {stride: span_ns})."""
+                  static_ratio: float = 0.0, num_slots: int = 2, link_slowdown: float = 1.0,
+                  rates: "HostRates | None" = None, placement: Placement = Placement.STATIC_LAST):
+    """Stride with the smallest predicted B200 span; returns (stride, {stride: span_ns}).
+    With measured ``rates`` the prediction is the fluid host-DRAM model
+    (``simulate_b200_fluid``), else the list-scheduled ``simulate_b200_phase``."""
     n = len(sizes)
     spans = {}
     for k in candidates:
-        plan = _quiet_plan(n, k, static_ratio)
-        spans[k] = simulate_b200_phase(plan, profile, list(sizes), num_slots, link_slowdown).span_ns
+        plan = _quiet_plan(n, k, static_ratio, placement)
+        if rates is not None:
+            spans[k] = simulate_b200_fluid(plan, list(sizes), link_bytes_per_s=rates.link_bytes_per_s,
+                                           host_params_per_s=rates.host_params_per_s,
+                                           fast_params_per_s=rates.fast_params_per_s,
+                                           host_dram_bytes_per_s=rates.host_dram_bytes_per_s, num_slots=num_slots)
+        else:
+            spans[k] = simulate_b200_phase(plan, profile, list(sizes), num_slots, link_slowdown).span_ns
     best = min(spans, key=lambda k: (spans[k], 0 if k is ALL_CPU else k))
     return best, spans
 
@@ -169,11 +192,13 @@ class StrideTuner:
     def __init__(self, profile: SystemProfile, sizes: Sequence[int], candidates: Iterable = range(1, 7),
                  static_ratio: float = 0.0, explore: int = 4, num_slots: int = 2,
                  link_slowdown: float = 1.0, hill_climb: bool = True,
-                 placement: Placement = Placement.STATIC_LAST, refine: bool = True) -> None:
+                 placement: Placement = Placement.STATIC_LAST, refine: bool = True,
+                 rates: "HostRates | None" = None) -> None:
         self.sizes = list(sizes)
         self.static_ratio = static_ratio
         self.placement = placement
-        best, spans = choose_stride(profile, self.sizes, candidates, static_ratio, num_slots, link_slowdown)
+        best, spans = choose_stride(profile, self.sizes, candidates, static_ratio, num_slots, link_slowdown,
+                                    rates, placement)
         ranked = sorted(spans, key=lambda k: spans[k])
         self.queue = ranked[:max(1, explore)]
         self.predicted = spans
@@ -236,3 +261,95 @@ def capacity_static_ratio(sizes: Sequence[int], free_hbm_bytes: int, *, lowp_byt
     if count == n:  # nothing streams: no windows needed
         count = n if free_hbm_bytes - headroom_bytes - (lowp_bytes_per_param + 12) * sum(sizes) >= 0 else n - 1
     return count / n
+
+
+def simulate_b200_fluid(plan: UpdatePlan, sizes: Sequence[int], *, link_bytes_per_s: float,
+                        host_params_per_s: float, fast_params_per_s: float, host_dram_bytes_per_s: float,
+                        num_slots: int = 2) -> int:
+    """Predicted span (ns) of ``plan`` on the B200 engine with the host DRAM
+    modelled as a shared resource.
+
+    Same lanes, FIFO order, dependencies and window gating as
+    ``simulate_b200_phase``, but rates are fluid: every action runs at its
+    own cap (the link per direction for copies, the uncontended H1 rate for
+    host updates, K1 for GPU updates) unless the host-DRAM traffic of the
+    actions running together exceeds the measured host-DRAM peak, in which
+    case every DRAM consumer is slowed by the same factor (what the probes
+    measure: under duplex DMA both H1 and the copy engines drop to ~0.6 of
+    their solo rates).  Host bytes per param: 12 per fp32 piece moved over
+    the link (4 per piece), 2 per half-precision copy, 28 per host update
+    (fused working-copy store)."""
+    sizes = list(sizes)
+    acts = plan.actions
+    n = len(acts)
+    dyn = set(plan.dynamic_fast)
+    # per action: lane, work units, cap (units/s), host DRAM bytes per unit
+    work, cap, dram = [0.0] * n, [1.0] * n, [0.0] * n
+    for a in acts:
+        k, s = a.kind, (sizes[a.subgroup] if a.subgroup >= 0 else 0)
+        if k in _H2D_STATE or k in _D2H_STATE:
+            work[a.id], cap[a.id], dram[a.id] = 4.0 * s, link_bytes_per_s, 1.0
+        elif k is ActionKind.H2D_PARAMS16:
+            work[a.id], cap[a.id], dram[a.id] = 2.0 * s, link_bytes_per_s, 1.0
+        elif k is ActionKind.CPU_UPDATE:
+            work[a.id], cap[a.id], dram[a.id] = float(s), host_params_per_s, 28.0
+        elif k is ActionKind.GPU_UPDATE:
+            work[a.id], cap[a.id] = float(s), fast_params_per_s
+    queues: dict = {lane: [] for lane in Lane}
+    for a in acts:
+        queues[a.lane].append(a.id)
+    head = dict.fromkeys(Lane, 0)
+    finish: list = [None] * n
+    window_no: dict[int, int] = {}  # subgroup -> index of its window, in opening order
+    closes: list = []               # finish time of each window's FLUSH_OUT_P (None until it happens)
+    running: dict = {}              # lane -> [action id, remaining work]
+    t = 0.0
+    done = 0
+    while done < n:
+        progressed = True
+        while progressed:  # start every lane head whose deps and window are satisfied (zero-work ones finish now)
+            progressed = False
+            for lane, q in queues.items():
+                if lane in running or head[lane] >= len(q):
+                    continue
+                aid = q[head[lane]]
+                a = acts[aid]
+                if any(finish[d] is None or finish[d] > t for d in a.deps):
+                    continue
+                if a.kind is ActionKind.PREFETCH_M and a.subgroup in dyn and a.subgroup not in window_no:
+                    w = len(closes)
+                    if w >= num_slots and (closes[w - num_slots] is None or closes[w - num_slots] > t):
+                        continue
+                    window_no[a.subgroup] = w
+                    closes.append(None)
+                head[lane] += 1
+                if work[aid] <= 0:
+                    finish[aid] = t
+                    done += 1
+                    if a.kind is ActionKind.FLUSH_OUT_P and a.subgroup in window_no:
+                        closes[window_no[a.subgroup]] = t
+                else:
+                    running[lane] = [aid, work[aid]]
+                progressed = True
+        if not running:
+            if done < n:
+                raise RuntimeError("fluid simulation stalled (plan order not executable)")
+            break
+        demand = sum(dram[aid] * cap[aid] for aid, _ in running.values())
+        f = min(1.0, host_dram_bytes_per_s / demand) if demand > 0 else 1.0
+        rate = {lane: cap[aid] * (f if dram[aid] > 0 else 1.0) for lane, (aid, _) in running.items()}
+        dt = min(rem / rate[lane] for lane, (_, rem) in running.items())
+        t += dt
+        for lane in list(running):
+            aid, rem = running[lane]
+            rem -= rate[lane] * dt
+            if rem <= 1e-9 * max(1.0, work[aid]):
+                finish[aid] = t
+                done += 1
+                a = acts[aid]
+                if a.kind is ActionKind.FLUSH_OUT_P and a.subgroup in window_no:
+                    closes[window_no[a.subgroup]] = t
+                del running[lane]
+            else:
+                running[lane][1] = rem
+    return int(round(max(finish) * 1e9)) if n else 0

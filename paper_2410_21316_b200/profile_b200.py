@@ -268,6 +268,21 @@ def measure_host_dram(nbytes: int = 1 << 31, reps: int = 3, with_dma: bool = Tru
     return out
 
 
+def host_rates():
+    """``policy.HostRates`` from the last ``measure_profile`` (None before one)."""
+    from .policy import HostRates
+
+    raw = LAST_RAW
+    if not raw:
+        return None
+    return HostRates(link_bytes_per_s=raw["link"]["duplex_GBs_per_dir"] * 1e9,
+                     host_params_per_s=raw["h1_alone"]["h1_params_per_s"],
+                     fast_params_per_s=raw["k1"]["k1_params_per_s"],
+                     host_dram_bytes_per_s=max(raw.get("host_dram", {}).get("peak_GBs", 0.0),
+                                               raw["h1_with_dma"].get("host_dram_GBs_combined", 0.0),
+                                               raw["h1_alone"]["h1_GBs"]) * 1e9)
+
+
 def measure_profile(fast_capacity_bytes: int | None = None, save: bool = False, quick: bool = False) -> SystemProfile:
     """Measure all planner constants on this box; returns a SystemProfile."""
     n = 25_000_000 if quick else 100_000_000

@@ -400,3 +400,52 @@ def test_capacity_static_ratio():
     assert capacity_static_ratio([sg] * 70, free) == 1.0  # 7B: every subgroup resident
     assert capacity_static_ratio([sg] * 10, 1 << 30) == 0.0
     assert capacity_static_ratio([], free) == 0.0
+
+
+def test_fluid_model_limits():
+    """simulate_b200_fluid: serial chains with no DRAM limit add up; all
+    residents cost n x S / K1; a host update alone over the DRAM limit runs
+    at peak / 28 B."""
+    from paper_2410_21316_b200.policy import simulate_b200_fluid
+
+    S, L, R, K = 10**8, 50e9, 6e9, 2e11
+    kw = dict(link_bytes_per_s=L, host_params_per_s=R, fast_params_per_s=K)
+    plan = build_plan(4, ALL_CPU)
+    t = simulate_b200_fluid(plan, [S] * 4, host_dram_bytes_per_s=float("inf"), **kw)
+    assert t == pytest.approx(4 * (S / R + 2 * S / L) * 1e9, abs=2)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        plan = build_plan(5, 2, static_ratio=1.0)
+    assert simulate_b200_fluid(plan, [S] * 5, host_dram_bytes_per_s=1e9, **kw) == pytest.approx(5 * S / K * 1e9, abs=2)
+    plan = build_plan(1, ALL_CPU)
+    t = simulate_b200_fluid(plan, [S], host_dram_bytes_per_s=100e9, **kw)
+    assert t == pytest.approx((S * 28 / 100e9 + 2 * S / L) * 1e9, abs=2)
+
+
+def test_fluid_model_dram_sharing_and_tuner_ranking(h100):
+    """With a finite host-DRAM peak the interleaved plans slow down, more so
+    the more they stream and update on the host at once; the tuner orders
+    its exploration by the fluid prediction when given measured rates."""
+    from paper_2410_21316_b200 import policy
+
+    S = 10**8
+    rates = policy.HostRates(link_bytes_per_s=50e9, host_params_per_s=6.1e9, fast_params_per_s=2.2e11,
+                             host_dram_bytes_per_s=185e9)
+    free = dataclasses.replace(rates, host_dram_bytes_per_s=float("inf"))
+    for k in (2, 3, 4, 5):
+        plan = build_plan(70, k, static_ratio=0.2, placement=Placement.STATIC_FIRST)
+        kw = dict(link_bytes_per_s=50e9, host_params_per_s=6.1e9, fast_params_per_s=2.2e11)
+        shared = policy.simulate_b200_fluid(plan, [S] * 70, host_dram_bytes_per_s=185e9, **kw)
+        alone = policy.simulate_b200_fluid(plan, [S] * 70, host_dram_bytes_per_s=float("inf"), **kw)
+        assert shared > alone
+        # never faster than its total host traffic at the peak
+        fast = sum(1 for d in plan.devices if d is Device.FAST) - len(plan.static_set)
+        cpu = 70 - fast - len(plan.static_set)
+        assert shared >= (24 * fast + 30 * cpu) * S / 185e9 * 1e9 * 0.999
+    tuner = policy.StrideTuner(h100, [S] * 70, range(1, 7), 0.2, explore=2, rates=rates,
+                               placement=Placement.STATIC_FIRST)
+    ranked = sorted(tuner.predicted, key=tuner.predicted.get)
+    assert tuner.queue == ranked[:2] and tuner.predicted[1] > tuner.predicted[3]
+    _, spans_free = policy.choose_stride(h100, [S] * 70, range(1, 7), 0.2, rates=free,
+                                         placement=Placement.STATIC_FIRST)
+    assert all(spans_free[k] <= tuner.predicted[k] for k in spans_free)
