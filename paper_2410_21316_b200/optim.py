@@ -143,7 +143,12 @@ class DeepOptimizerStates:
         self.sizes = sizes
         self.tuner = None
         if stride == "auto":
-            self.tuner = policy.StrideTuner(profile, self.sizes, range(1, 7), static_ratio, explore=explore)
+            # measured host rates (profile_b200.measure_profile earlier in this process) let the
+            # fluid host-DRAM model order the exploration
+            from . import profile_b200
+
+            self.tuner = policy.StrideTuner(profile, self.sizes, range(1, 7), static_ratio, explore=explore,
+                                            rates=profile_b200.host_rates())
             if self.world > 1:  # the same exploration order on every rank
                 box = [self.tuner.queue]
                 dist.broadcast_object_list(box, src=0, group=process_group)

@@ -269,17 +269,24 @@ def measure_host_dram(nbytes: int = 1 << 31, reps: int = 3, with_dma: bool = Tru
 
 
 def host_rates():
-    """``policy.HostRates`` from the last ``measure_profile`` (None before one)."""
+    """``policy.HostRates`` from the last ``measure_profile`` in this process,
+    else from the committed measurement (``profiles/b200_node_profile.json``),
+    else None."""
     from .policy import HostRates
 
     raw = LAST_RAW
-    if not raw:
+    if not raw and _OUT.exists():
+        try:
+            raw = json.loads(_OUT.read_text()).get("raw", {})
+        except (OSError, ValueError):
+            raw = {}
+    if not raw or "link" not in raw or "h1_alone" not in raw or "k1" not in raw:
         return None
     return HostRates(link_bytes_per_s=raw["link"]["duplex_GBs_per_dir"] * 1e9,
                      host_params_per_s=raw["h1_alone"]["h1_params_per_s"],
                      fast_params_per_s=raw["k1"]["k1_params_per_s"],
                      host_dram_bytes_per_s=max(raw.get("host_dram", {}).get("peak_GBs", 0.0),
-                                               raw["h1_with_dma"].get("host_dram_GBs_combined", 0.0),
+                                               raw.get("h1_with_dma", {}).get("host_dram_GBs_combined", 0.0),
                                                raw["h1_alone"]["h1_GBs"]) * 1e9)
 
 
@@ -315,8 +322,8 @@ def measure_profile(fast_capacity_bytes: int | None = None, save: bool = False, 
                      "link_slowdown_under_h1": max(1.0, link["duplex_GBs_per_dir"] / link_h1["duplex_GBs_per_dir"])})
     if save:
         d = dataclasses.asdict(prof)
-        d["raw"] = {"link": link, "k1": k1, "h1_alone": h1_alone, "h1_with_dma": h1_busy,
-                    "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
+        d["raw"] = {"link": link, "k1": k1, "h1_alone": h1_alone, "h1_with_dma": h1_busy, "host_dram": dram,
+                    "link_under_h1": link_h1, "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
         _OUT.parent.mkdir(exist_ok=True)
         _OUT.write_text(json.dumps(d, indent=1))
     return prof
