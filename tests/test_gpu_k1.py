@@ -164,3 +164,31 @@ def test_k1_fused_broadcast_to_peers(npeers, n, off):
     for q in peers:
         assert q[off:off + n].cpu().numpy().view(np.uint16).tobytes() == want
         assert torch.count_nonzero(q[:off]) == 0 and torch.count_nonzero(q[off + n:]) == 0
+
+
+@pytest.mark.parametrize("gkind", ["fp32", "bf16"])
+def test_k1_non_finite_grads(gkind):
+    """Non-finite inputs (overflowed or NaN grads, an infinite moment): every
+    finite result is bit-identical to the oracle, and NaN appears exactly
+    where the oracle has NaN.  (The NaN *bit patterns* are not compared: the
+    GPU returns the canonical NaN while x86 propagates payloads — the
+    reference pins payloads only for its conversions.)"""
+    n = 4096 * 3 + 77
+    p, m, v, g32 = _inputs(n, 11)
+    rng = np.random.default_rng(12)
+    idx = rng.choice(n, 200, replace=False)
+    g32[idx[:50]] = np.inf
+    g32[idx[50:100]] = -np.inf
+    g32[idx[100:150]] = np.nan
+    g32[idx[150:175]] = 3e38  # finite, but g*g overflows in fp32
+    m[idx[175:]] = np.inf
+    g, gw = _grads_of(g32, gkind)
+    hyper = (1e-3, 0.9, 0.999, 1e-8)
+    got = _run_k1(p.copy(), m.copy(), v.copy(), g, gkind, "bf16", n, 0, hyper, 3)
+    wp, wm, wv = p.copy(), m.copy(), v.copy()
+    O.adam_step(wp, wm, wv, gw, *hyper, 3)
+    for a, b in zip(got[:3], (wp, wm, wv)):
+        nan_a, nan_b = np.isnan(a), np.isnan(b)
+        assert np.array_equal(nan_a, nan_b)
+        assert np.array_equal(a[~nan_a].view(np.uint32), b[~nan_b].view(np.uint32))
+    assert np.isnan(wp).any() and np.isinf(wm).any()  # the cases really happened
