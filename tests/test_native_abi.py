@@ -57,6 +57,31 @@ def test_adam_step_arrays_host_bit_exact(n, step):
     assert p.tobytes() == rp.tobytes() and m.tobytes() == rm.tobytes() and v.tobytes() == rv.tobytes()
 
 
+def test_host_adam_non_finite_inputs():
+    """H1 with overflowed / NaN grads and infinite moments: finite results
+    bit-exact, NaN at the oracle's positions (NaN bits are not compared)."""
+    import warnings
+
+    n = 100_003
+    p, m, v, g = _state(n, 5)
+    rng = np.random.default_rng(6)
+    idx = rng.choice(n, 400, replace=False)
+    g[idx[:100]] = np.inf
+    g[idx[100:200]] = np.nan
+    g[idx[200:300]] = 3e38
+    m[idx[300:]] = -np.inf
+    rp, rm, rv = p.copy(), m.copy(), v.copy()
+    D.adam_step_arrays(p, m, v, g, 1e-3, 0.9, 0.999, 1e-8, 2)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", RuntimeWarning)
+        O.adam_step(rp, rm, rv, g, 1e-3, 0.9, 0.999, 1e-8, 2)
+    for a, b in ((p, rp), (m, rm), (v, rv)):
+        assert np.array_equal(np.isnan(a), np.isnan(b))
+        ok = ~np.isnan(a)
+        assert a[ok].tobytes() == b[ok].tobytes()
+    assert np.isnan(rp).any()
+
+
 @pytest.mark.parametrize("lowp", ["fp16", "bf16"])
 @pytest.mark.parametrize("wd", [0.0, 0.01])
 def test_host_fused_lowp_grads_and_working_copy(lowp, wd):
