@@ -748,7 +748,12 @@ class B200Bench:
             "planner_k": "all_cpu" if self.choice.k is D.ALL_CPU else self.choice.k, "k_real": self.choice.k_real,
             "predicted_span_ms_by_stride": None if self.stride_spans is None else
             {str(k): v / 1e6 for k, v in self.stride_spans.items()},
-            "measured_span_ms_by_stride": self.tuned, "static_ratio": r, "placement": self.placement.value,
+            "measured_span_ms_by_stride": self.tuned,
+            # the fluid host-DRAM model's error where it was checked by measurement
+            "model_error_pct_by_stride": None if not (self.stride_spans and self.tuned) else
+            {k: round(100.0 * (self.stride_spans[int(k)] / 1e6 - v) / v, 2) for k, v in self.tuned.items()
+             if int(k) in self.stride_spans},
+            "static_ratio": r, "placement": self.placement.value,
             "fast_capacity_bytes": self.cap, "hbm_windows": windows,
             "parallelism": f"zero3-shard{self.world}", "l2": "inputs > L2 (28 B/param over 1e8-param subgroups)"}
         line = {"metric": METRIC, "value": self.P / (self.ms * 1e-3), "unit": UNIT, "n_gpus": self.world,
