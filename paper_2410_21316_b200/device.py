@@ -491,3 +491,48 @@ class B200Target(SimTarget):
         acts = self.plan.actions
         return tuple(ScheduledAction(action=acts[i], start_ns=int(s[i]), end_ns=int(e[i]),
                                      bytes=self.bytes_of(acts[i])) for i in range(n))
+
+
+def load_shard(params32, momentum32, variance32, grads16, model16, subgroup_size: int, *, lowp: str = "bf16",
+               static_set=frozenset(), device=None) -> ShardedOptimizer:
+    """A B200-attached shard built from whole-shard arrays, each subgroup
+    written straight to its home: the static residents' fp32 state into their
+    HBM allocations (no host memory for it: sparse pinned pool), everyone
+    else's into the pinned pool; grads and working copy to HBM (and to the
+    host images of host-homed subgroups).
+
+    ``params32``/``momentum32``/``variance32``: float32 arrays (numpy or CPU
+    torch); ``grads16``/``model16``: the half-precision kind's bits (numpy
+    float16 for fp16, uint16 bf16 bits for bf16)."""
+    torch = _torch()
+    p, m, v = (np.ascontiguousarray(np.asarray(x, dtype=np.float32)).reshape(-1)
+               for x in (params32, momentum32, variance32))
+    want16 = np.dtype(np.float16) if lowp == "fp16" else np.dtype(np.uint16)
+    g, w = (np.ascontiguousarray(np.asarray(x)).reshape(-1) for x in (grads16, model16))
+    total = p.size
+    for name, a, dt in (("momentum32", m, np.float32), ("variance32", v, np.float32), ("grads16", g, want16),
+                        ("model16", w, want16)):
+        if a.size != total:
+            raise ValueError(f"{name} must hold {total} elements")
+        if a.dtype != dt:
+            raise TypeError(f"{name} must be {np.dtype(dt)}, got {a.dtype}")
+    static_set = frozenset(int(i) for i in static_set)
+    nsg = -(-total // int(subgroup_size))
+    if any(i < 0 or i >= nsg for i in static_set):
+        raise ValueError(f"static subgroups must be in [0, {nsg})")
+    opt = ShardedOptimizer.allocate(total, subgroup_size, lowp=lowp, host_homed=[i for i in range(nsg)
+                                                                                  if i not in static_set])
+    for a, b in opt.host_runs("state"):
+        opt._p[a:b], opt._m[a:b], opt._v[a:b] = p[a:b], m[a:b], v[a:b]
+    for a, b in opt.host_runs("lowp"):
+        opt._g[a:b], opt._w[a:b] = g[a:b], w[a:b]
+    res = opt.to_device(device)
+    res.set_static(static_set)
+    i16 = lambda x: torch.from_numpy(x.view(np.int16))
+    for i in sorted(static_set):
+        sl = opt.subgroups[i].slice
+        for t, src in zip(res.static_views(i), (p, m, v)):
+            t.copy_(torch.from_numpy(src[sl]))
+        res.grads.view(torch.int16)[sl].copy_(i16(g[sl]))
+        res.model16.view(torch.int16)[sl].copy_(i16(w[sl]))
+    return opt

@@ -41,29 +41,10 @@ def _plan(n, s):
     return D.build_plan(n, s["stride"], s["ratio"], s["placement"])
 
 
-def _t(a):
-    return torch.from_numpy(a.view(np.int16) if a.itemsize == 2 else a)
-
-
 def _sparse(total, sg, seed, lowp, static):
-    """The oracle's shard in a sparse pool: host memory only for the first
-    plan's host-homed subgroups, residents written straight into HBM."""
+    """The oracle's shard in a sparse pool: residents homed in HBM only."""
     ref = O.initialize(total, sg, seed, lowp)
-    n = -(-total // sg)
-    opt = D.ShardedOptimizer.allocate(total, sg, lowp=lowp, host_homed=[i for i in range(n) if i not in static])
-    for a, b in opt.host_runs("state"):
-        opt._p[a:b], opt._m[a:b], opt._v[a:b] = ref["p"][a:b], ref["m"][a:b], ref["v"][a:b]
-    for a, b in opt.host_runs("lowp"):
-        opt._g[a:b], opt._w[a:b] = ref["g"][a:b], ref["w"][a:b]
-    res = opt.to_device()
-    res.set_static(static)
-    for i in static:
-        g = opt.subgroups[i]
-        for t, key in zip(res.static_views(i), "pmv"):
-            t.copy_(_t(ref[key][g.slice]))
-        res.grads.view(torch.int16)[g.slice].copy_(_t(ref["g"][g.slice]))
-        res.model16.view(torch.int16)[g.slice].copy_(_t(ref["w"][g.slice]))
-    return opt
+    return D.load_shard(ref["p"], ref["m"], ref["v"], ref["g"], ref["w"], sg, lowp=lowp, static_set=static)
 
 
 def test_random_engine_options_match_oracle(h100):

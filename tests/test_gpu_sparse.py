@@ -19,28 +19,11 @@ from paper_2410_21316_b200 import Placement  # noqa: E402
 HYPER = D.AdamHyper()
 
 
-def _t(a: np.ndarray):
-    return torch.from_numpy(a.view(np.int16) if a.itemsize == 2 else a)
-
-
 def sparse_shard(total, sg, seed, lowp, static_set):
-    """The oracle's seeded shard, loaded into a sparse pool whose static
-    residents are written straight into their HBM homes."""
+    """The oracle's seeded shard, loaded with its static residents homed in
+    HBM only (D.load_shard: sparse pinned pool)."""
     want = O.initialize(total, sg, seed, lowp)
-    nsg = math.ceil(total / sg)
-    opt = D.ShardedOptimizer.allocate(total, sg, lowp=lowp, host_homed=[i for i in range(nsg) if i not in static_set])
-    for a, b in opt.host_runs("state"):
-        opt._p[a:b], opt._m[a:b], opt._v[a:b] = want["p"][a:b], want["m"][a:b], want["v"][a:b]
-    for a, b in opt.host_runs("lowp"):
-        opt._g[a:b], opt._w[a:b] = want["g"][a:b], want["w"][a:b]
-    res = opt.to_device()
-    res.set_static(frozenset(static_set))
-    for i in static_set:
-        g = opt.subgroups[i]
-        for t, key in zip(res.static_views(i), "pmv"):
-            t.copy_(_t(want[key][g.slice]))
-        res.grads.view(torch.int16)[g.slice].copy_(_t(want["g"][g.slice]))
-        res.model16.view(torch.int16)[g.slice].copy_(_t(want["w"][g.slice]))
+    opt = D.load_shard(want["p"], want["m"], want["v"], want["g"], want["w"], sg, lowp=lowp, static_set=static_set)
     return opt, want
 
 

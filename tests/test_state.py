@@ -240,3 +240,16 @@ def test_host_membw_probe():
     for bad in ((a.address, b.address, 1 << 22, 2), (a.address, None, 1 << 22, 1), (None, b.address, 64, 0)):
         with pytest.raises(ValueError):
             N.check(N.lib().dos_host_membw(*bad, 0, ctypes.byref(secs)))
+
+
+def test_load_shard_validates_before_touching_a_device():
+    from paper_2410_21316_b200.device import load_shard
+
+    n = 1000
+    f32, u16 = np.zeros(n, np.float32), np.zeros(n, np.uint16)
+    with pytest.raises(TypeError):
+        load_shard(f32, f32, f32, f32, u16, 100)  # grads must be bf16 bits
+    with pytest.raises(ValueError):
+        load_shard(f32, f32[:-1], f32, u16, u16, 100)
+    with pytest.raises(ValueError):
+        load_shard(f32, f32, f32, u16, u16, 100, static_set={10})
