@@ -99,6 +99,22 @@ int dos_adam_step_cuda_rs(float* p, float* m, float* v, const void* const* g_src
 int dos_reduce_scatter_cuda(void* out, const void* const* src, int nsrc, int dtype, float scale,
                             int64_t n, void* stream);
 
+/* ---- Post-phase coherence (executor.py:271-282: model16 == downscale_rne(params32)
+ * for every subgroup, asserted after each phase).  Each range compares
+ * lowp[i] with RNE(p32[i]) in `nwin` windows of `window` elements: the whole
+ * range when nwin*window >= n, else windows spread evenly from its first
+ * element to its last (a sample).  p32/lowp may be HBM or registered pinned
+ * host memory.  Asynchronous on `stream`; out (device, 2 x u64, caller
+ * initialises to {0, ~0}) receives the mismatch count and the smallest
+ * (range_index << 40 | element) key. */
+typedef struct dos_coh_range {
+  const float* p32;
+  const void* lowp;
+  int64_t n, window, nwin;
+} dos_coh_range;
+int dos_coherence_cuda(const dos_coh_range* ranges, int nranges, int lowp_dtype,
+                       unsigned long long* out, void* stream);
+
 /* ---- CUDA IPC for symmetric full-model buffers (one process per GPU).
  * export: the handle of the allocation containing dev_ptr and dev_ptr's
  * byte offset in it; import: map a peer's allocation (cached) and return

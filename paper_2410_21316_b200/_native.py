@@ -85,6 +85,11 @@ class dos_action_desc(C.Structure):
     ]
 
 
+class dos_coh_range(C.Structure):
+    _fields_ = [("p32", C.c_void_p), ("lowp", C.c_void_p), ("n", C.c_int64), ("window", C.c_int64),
+                ("nwin", C.c_int64)]
+
+
 # every symbol include/dos.h declares, with its ctypes signature
 _VP, _I, _I64, _SZ = C.c_void_p, C.c_int, C.c_int64, C.c_size_t
 SIGNATURES: dict[str, tuple] = {
@@ -98,6 +103,7 @@ SIGNATURES: dict[str, tuple] = {
     "dos_adam_step_cuda_rs": (_I, [_VP, _VP, _VP, C.POINTER(_VP), _I, _I, _I, C.c_float, _VP, _I, C.POINTER(_VP),
                                    _I, _I64, C.POINTER(dos_adam_scalars), _VP]),
     "dos_reduce_scatter_cuda": (_I, [_VP, C.POINTER(_VP), _I, _I, C.c_float, _I64, _VP]),
+    "dos_coherence_cuda": (_I, [C.POINTER(dos_coh_range), _I, _I, C.POINTER(C.c_ulonglong), _VP]),
     "dos_ipc_export": (_I, [_VP, C.c_char_p, C.POINTER(C.c_uint64)]),
     "dos_ipc_import": (_I, [C.c_char_p, C.c_uint64, C.POINTER(_VP)]),
     "dos_ipc_close_all": (_I, []),

@@ -919,3 +919,103 @@ extern "C" int dos_adam_step_cuda_rs(float* p, float* m, float* v, const void* c
   return dos_adam_launch(p, m, v, gs.p[self], g_dtype, p_lowp, lowp_dtype, n, dos_make_kscal(s),
                          reinterpret_cast<cudaStream_t>(stream), pr, gs);
 }
+
+// ---------------------------------------------------------------- coherence
+// The reference's post-phase guarantee (executor.py:271-282): every
+// subgroup's half-precision params equal downscale(params32), bit for bit.
+// One launch checks a batch of ranges; each range is read in `nwin` windows
+// of `window` elements — contiguous (the whole range) when nwin*window >= n,
+// else spread evenly from the first element to the last (a sample).  p32 and
+// the working copy may live in HBM or in mapped pinned host memory (device
+// aliases resolved by the caller).  Mismatches are counted in out[0] and the
+// smallest (range << 40 | element) key is kept in out[1].
+namespace {
+constexpr int kCohMax = 160;  // ranges per launch (7.7 KB of kernel parameters)
+struct coh_batch {
+  int n;
+  int lt;
+  int base;  // index of range 0 of this batch in the caller's list
+  const float* p[kCohMax];
+  const uint16_t* w[kCohMax];
+  int64_t len[kCohMax], win[kCohMax], nwin[kCohMax], first[kCohMax + 1];
+};
+
+__global__ void __launch_bounds__(kThreads) k_coherence(const __grid_constant__ coh_batch b,
+                                                         unsigned long long* out) {
+  const int64_t total = b.first[b.n];
+  for (int64_t pair = blockIdx.x; pair < total; pair += gridDim.x) {
+    int lo = 0, hi = b.n - 1;  // range r with first[r] <= pair < first[r+1]
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (b.first[mid] <= pair) lo = mid; else hi = mid - 1;
+    }
+    const int r = lo;
+    const int64_t k = pair - b.first[r], n = b.len[r], win = b.win[r], nw = b.nwin[r];
+    const int64_t start = nw * win >= n ? k * win : (nw > 1 ? k * (n - win) / (nw - 1) : 0);
+    const int64_t stop = start + win < n ? start + win : n;
+    unsigned long long bad = 0, key = ~0ull;
+    for (int64_t i = start + threadIdx.x; i < stop; i += kThreads) {
+      if (to_lowp(b.p[r][i], b.lt) != b.w[r][i]) {
+        ++bad;
+        const unsigned long long kk = ((unsigned long long)(b.base + r) << 40) | (unsigned long long)i;
+        key = kk < key ? kk : key;
+      }
+    }
+    if (bad) {
+      atomicAdd(out, bad);
+      atomicMin(out + 1, key);
+    }
+  }
+}
+
+const void* device_alias(const void* ptr) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return ptr;
+  if (a.type == cudaMemoryTypeHost) return a.devicePointer;  // registered / pinned host memory
+  return nullptr;  // pageable: not readable by the device
+}
+}  // namespace
+
+extern "C" int dos_coherence_cuda(const dos_coh_range* ranges, int nranges, int lowp_dtype,
+                                  unsigned long long* out, void* stream) {
+  if (nranges < 0 || (nranges > 0 && (!ranges || !out))) return dos_set_error(DOS_EINVAL, "bad coherence arguments");
+  if (lowp_dtype != DOS_F16 && lowp_dtype != DOS_BF16)
+    return dos_set_error(DOS_ETYPE, "working-copy dtype %d unsupported", lowp_dtype);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  for (int base = 0; base < nranges; base += kCohMax) {
+    coh_batch b;
+    b.n = 0;
+    b.lt = lowp_dtype;
+    b.base = base;
+    b.first[0] = 0;
+    for (int j = base; j < nranges && b.n < kCohMax; ++j) {
+      const dos_coh_range& r = ranges[j];
+      if (r.n < 0 || r.window <= 0 || r.nwin <= 0) return dos_set_error(DOS_EINVAL, "coherence range %d: bad sizes", j);
+      const void* p = device_alias(r.p32);
+      const void* w = device_alias(r.lowp);
+      if (r.n > 0 && (!p || !w))
+        return dos_set_error(DOS_EINVAL, "coherence range %d: buffer not device-accessible (pageable host memory?)", j);
+      const int i = b.n++;
+      b.p[i] = static_cast<const float*>(p);
+      b.w[i] = static_cast<const uint16_t*>(w);
+      b.len[i] = r.n;
+      b.win[i] = r.window < r.n ? r.window : (r.n > 0 ? r.n : 1);
+      // whole range: enough contiguous windows to cover it
+      const int64_t need = (r.n + b.win[i] - 1) / b.win[i];
+      b.nwin[i] = r.n == 0 ? 0 : (r.nwin < need ? r.nwin : need);
+      b.first[i + 1] = b.first[i] + b.nwin[i];
+    }
+    const int64_t pairs = b.first[b.n];
+    if (pairs == 0) continue;
+    const unsigned grid = (unsigned)(pairs < (int64_t)sm_count() * 8 ? pairs : (int64_t)sm_count() * 8);
+    k_coherence<<<grid, kThreads, 0, st>>>(b, out);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return dos_set_error(DOS_ECUDA, "coherence launch failed: %s", cudaGetErrorString(e));
+  }
+  return DOS_OK;
+}

@@ -26,6 +26,7 @@
 #include <string>
 #include <thread>
 #include <map>
+#include <memory>
 #include <unordered_map>
 #include <vector>
 
@@ -146,8 +147,12 @@ class Team {
   bool stop_ = false;
 };
 
+// The team is shared: every parallel section holds a reference for its
+// duration, so a resize (dos_set_host_threads) while the engine's host lane or
+// a pool commit is inside Team::run only swaps the global pointer; the old
+// team is destroyed (its workers joined) when its last user releases it.
 std::mutex g_team_mu;
-Team* g_team = nullptr;
+std::shared_ptr<Team> g_team;
 int g_team_want = 0;
 
 int default_threads() {
@@ -157,16 +162,17 @@ int default_threads() {
   return std::max(1, (int)std::thread::hardware_concurrency());
 }
 
-Team& team() {
+std::shared_ptr<Team> team() {
   std::lock_guard<std::mutex> lk(g_team_mu);
-  if (!g_team) g_team = new Team(g_team_want > 0 ? g_team_want : default_threads());
-  return *g_team;
+  if (!g_team) g_team = std::make_shared<Team>(g_team_want > 0 ? g_team_want : default_threads());
+  return g_team;
 }
 
 // Splits [0, n) into k chunks aligned to 64 elements (256 B of fp32).
 template <class F>
 void parallel_chunks(int64_t n, int nthreads, F&& body) {
-  Team& tm = team();
+  const std::shared_ptr<Team> hold = team();  // alive until this section returns
+  Team& tm = *hold;
   int k = nthreads > 0 ? std::min(nthreads, tm.size()) : tm.size();
   const int64_t min_chunk = 1 << 16;  // below this, threading costs more than it saves
   k = (int)std::max<int64_t>(1, std::min<int64_t>(k, (n + min_chunk - 1) / min_chunk));
@@ -182,15 +188,13 @@ void parallel_chunks(int64_t n, int nthreads, F&& body) {
 }
 }  // namespace
 
-extern "C" int dos_host_threads(void) { return team().size(); }
+extern "C" int dos_host_threads(void) { return team()->size(); }
 
 extern "C" int dos_set_host_threads(int n) {
   std::lock_guard<std::mutex> lk(g_team_mu);
   g_team_want = n;
-  if (g_team && g_team->size() != (n > 0 ? n : default_threads())) {
-    delete g_team;
-    g_team = nullptr;
-  }
+  if (g_team && g_team->size() != (n > 0 ? n : default_threads()))
+    g_team.reset();  // users still inside a section keep the old team alive
   return DOS_OK;
 }
 

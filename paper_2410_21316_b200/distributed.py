@@ -7,8 +7,10 @@ data path.  Around it:
 
 * before: **reduce-scatter** of the bf16 grads — fused into the phase
   (``PeerGrads``: K1 sums every rank's grads of the shard over NVLink as it
-  streams the state), or bucketed NCCL per subgroup index j (bucket j =
-  every rank's subgroup j; each rank receives its own);
+  streams the state), or bucketed per subgroup index j (bucket j = every
+  rank's subgroup j; an NCCL all-to-all hands each rank its pieces, summed
+  locally in rank order) — both with the same rounding, so the two modes
+  train to the same bits;
 * after: **all-gather** of the bf16 working copy, bucketed the same way.
   ``gather_params_overlapped`` makes a comm stream wait on the *engine event*
   of the action that finalises subgroup j's working copy (its GPU_UPDATE, or
@@ -18,8 +20,8 @@ data path.  Around it:
 Full-model buffers use the model's flat (rank-major) layout padded to
 ``N * ceil(P/N)``; the last rank's missing tail is zero padding so every
 collective has equal counts.  NCCL over NVLink/NVSwitch is the product
-backend; the same code runs on gloo (CPU tests), where reduce-scatter is
-emulated by all-reduce + slice.
+backend; the same code runs on gloo (CPU tests; 16-bit tensors exchanged as
+raw bits).
 """
 
 from __future__ import annotations
@@ -91,24 +93,38 @@ class BucketedCollectives:
         return [full[self.layout.global_offset(r, start): self.layout.global_offset(r, start) + size]
                 for r in range(self.world)]
 
-    def reduce_scatter_bucket(self, full_grads, out, j: int, op=None):
-        """Sum bucket j of every rank's full-model grads into ``out`` (this
-        rank's piece of bucket j, length = bucket size)."""
+    def reduce_scatter_bucket(self, full_grads, out, j: int, scale: float = 1.0) -> None:
+        """Bucket j of the grad reduce-scatter: ``out`` (this rank's piece of
+        bucket j) = the rank-order sum of every rank's grads for it, with the
+        declared rounding of ``oracle.reduce_scatter`` / ``dos_gsrc`` (fp32
+        adds in rank order, one rounding to the grad dtype, then the scale
+        rounded once more) — bit-identical to the reduce-scatter fused into
+        the phase (``PeerGrads``).
+
+        The collective only moves bytes: an all-to-all hands each rank every
+        rank's 16-bit piece of its shard (the same (N-1)/N traffic as a ring
+        reduce-scatter, over NVLink under NCCL), and the sum runs on this
+        rank in rank order (``dos_reduce_scatter_cuda``).  A reduction inside
+        NCCL would add in its own order and round in 16 bits at every hop."""
         import torch
         import torch.distributed as dist
 
-        op = dist.ReduceOp.SUM if op is None else op
         views = self._views(full_grads, j)
-        if self.backend == "nccl":
-            return dist.reduce_scatter(out, views, op=op, group=self.group, async_op=True)
-        # gloo: no reduce-scatter and no 16-bit float support; all-reduce the
-        # bucket in fp32 (exact widening, one rounding back) and keep our piece
-        buf = torch.cat(views)
-        wide = buf.float() if buf.element_size() == 2 else buf
-        dist.all_reduce(wide, op=op, group=self.group)
         size = views[0].numel()
-        out.copy_(wide[self.rank * size:(self.rank + 1) * size].to(out.dtype))
-        return None
+        if out.numel() != size:
+            raise ValueError(f"bucket {j} piece has {size} elements, out has {out.numel()}")
+        if out.element_size() != 2:
+            raise TypeError("the grads must be half precision")
+        recv = torch.empty(self.world * size, dtype=out.dtype, device=out.device)
+        parts = list(recv.split(size))
+        if self.backend == "nccl":
+            dist.all_to_all(parts, [v.contiguous() for v in views], group=self.group)
+        else:  # gloo: 16-bit floats unsupported and CUDA tensors staged: exchange the raw bits on the host
+            send = torch.cat([v.contiguous().view(torch.uint8).cpu() for v in views])
+            got = torch.empty_like(send)
+            dist.all_to_all_single(got, send, group=self.group)
+            recv.view(torch.uint8).copy_(got)
+        reduce_in_rank_order(parts, out, scale)
 
     def all_gather_bucket(self, full_params, mine, j: int):
         """Every rank's piece of bucket j into the full-model buffer."""
@@ -129,17 +145,14 @@ class BucketedCollectives:
             dist.all_gather(views, src, group=self.group)
         return None
 
-    def reduce_scatter_all(self, full_grads, shard_grads, scale: float | None = None):
-        """All buckets; ``shard_grads`` is this rank's padded share (per_rank)."""
-        works = []
+    def reduce_scatter_all(self, full_grads, shard_grads, scale: float | None = None) -> None:
+        """All buckets; ``shard_grads`` is this rank's padded share (per_rank).
+        ``scale`` (e.g. 1/N to average) is applied inside the reduction, with
+        the fused path's rounding."""
         for j in range(self.layout.num_buckets):
             start, size = self.layout.bucket_span(j)
-            works.append(self.reduce_scatter_bucket(full_grads, shard_grads[start:start + size], j))
-        for w in works:
-            if w is not None:
-                w.wait()
-        if scale is not None:
-            shard_grads.mul_(scale)
+            self.reduce_scatter_bucket(full_grads, shard_grads[start:start + size], j,
+                                       1.0 if scale is None else float(scale))
 
     def all_gather_all(self, full_params, shard_params):
         works = []
@@ -149,6 +162,33 @@ class BucketedCollectives:
         for w in works:
             if w is not None:
                 w.wait()
+
+
+def reduce_in_rank_order(parts, out, scale: float = 1.0) -> None:
+    """``out`` = lowp(sum of ``parts`` in list order, fp32 RN adds), then
+    lowp(f32(that) * f32(scale)) if scale != 1 — ``oracle.reduce_scatter``'s
+    rule.  CUDA tensors: one ``dos_reduce_scatter_cuda`` launch on the
+    current stream (up to DOS_MAX_PEERS + 1 sources per launch); host tensors
+    (gloo CPU tests): the same arithmetic in torch."""
+    import ctypes as C
+
+    import torch
+
+    from . import _native as N
+
+    if out.is_cuda and len(parts) <= N.DOS_MAX_PEERS + 1:
+        dt = N.DOS_BF16 if out.dtype == torch.bfloat16 else N.DOS_F16
+        srcs = (C.c_void_p * len(parts))(*[p.data_ptr() for p in parts])
+        N.check(N.lib().dos_reduce_scatter_cuda(out.data_ptr(), srcs, len(parts), dt, float(scale), out.numel(),
+                                                torch.cuda.current_stream(out.device).cuda_stream))
+        return
+    acc = parts[0].float()
+    for p in parts[1:]:
+        acc = acc + p.float()  # fp32 RN, rank order
+    r = acc.to(out.dtype)  # RNE
+    if scale != 1.0:
+        r = (r.float() * torch.tensor(scale, dtype=torch.float32, device=r.device)).to(out.dtype)
+    out.copy_(r)
 
 
 def _ipc_bases(buf, group=None) -> dict[int, int]:

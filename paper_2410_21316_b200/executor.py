@@ -13,6 +13,7 @@
 
 from __future__ import annotations
 
+import ctypes as C
 import enum
 import math
 import time
@@ -179,7 +180,7 @@ def execute_plan(
     *,
     host_threads: int = 0,
     host_io: bool = False,
-    check_coherence: bool = False,
+    check_coherence: bool | str = "sampled",
     validate_measured: bool = True,
     on_submitted=None,
     peers=None,
@@ -191,9 +192,13 @@ def execute_plan(
 
     Same contract as executor.py:246-293: raises ValueError on a plan/shard
     size mismatch, audits the schedule, requires the staging windows to
-    drain, bumps ``step``.  ``check_coherence`` re-derives the working copy
-    from the fp32 params and compares bitwise (the reference always does;
-    here it is opt-in because it is a full extra pass).
+    drain, bumps ``step``, and asserts — as the reference always does
+    (executor.py:271-282) — that every subgroup's working copy equals the
+    downscaled fp32 params (``check_coherence_after_phase``; AssertionError
+    otherwise).  ``check_coherence``: ``"sampled"`` (default: HBM-homed
+    state compared in full on the device, host-homed state in evenly spread
+    windows of every subgroup read over the link), ``"full"`` / ``True``
+    (every element of every subgroup), ``"off"`` / ``False``.
 
     ``host_io=True`` is the host-buffer mode: this step's gradients are read
     from the host image (``grads16``) for every subgroup — fast subgroups
@@ -217,6 +222,7 @@ def execute_plan(
         raise ValueError(f"plan covers {plan.num_subgroups} subgroups, optimizer has {len(optimizer.subgroups)}")
     if mode is ExecMode.THROTTLED and throttle_scale <= 0:
         raise ValueError("throttle_scale must be positive")
+    coherence = _coherence_mode(check_coherence)
     step = optimizer.step + 1
     target = B200Target(profile, plan, optimizer, hyper, step, host_threads=host_threads, host_io=host_io,
                         peers=peers, flush_grads=flush_grads, fuse_downscale=fuse_downscale,
@@ -240,15 +246,107 @@ def execute_plan(
         validate_schedule(plan, measured_events, target, check_streams=False, max_windows=target.num_slots,
                           tolerance_ns=MEASURED_CLOCK_SLACK_NS)
     optimizer.step = step
-    if check_coherence:
-        w = optimizer.model16
-        want = lowp_downscale(optimizer.params32, optimizer.lowp)
-        for sg in optimizer.subgroups:
-            if want[sg.slice].tobytes() != w[sg.slice].tobytes():
-                raise AssertionError(f"model16 of subgroup {sg.index} incoherent with params32")
+    check_coherence_after_phase(optimizer, target.residency, coherence, host_io)
     if mode is ExecMode.THROTTLED:
         _pace_replay(timeline, throttle_scale)
     return ExecutionResult(optimizer=optimizer, timeline=timeline, step=step, mode=mode, measured=measured)
+
+
+# host-homed subgroups: this many windows of this many elements each, spread
+# from the first element to the last (ragged tails included), per subgroup
+COHERENCE_WINDOW = 2048
+COHERENCE_WINDOWS = 16
+
+
+def _coherence_mode(check) -> str:
+    if check is True:
+        return "full"
+    if check is False or check is None:
+        return "off"
+    if check not in ("full", "sampled", "off"):
+        raise ValueError(f"check_coherence must be 'sampled', 'full', 'off' or a bool, got {check!r}")
+    return check
+
+
+def check_coherence_after_phase(opt: ShardedOptimizer, res, mode: str = "sampled", host_io: bool = False) -> None:
+    """The reference's post-phase assertion (executor.py:271-282): for every
+    subgroup, model16 == downscale_rne(params32), bit for bit, else
+    AssertionError naming the first incoherent subgroup.
+
+    One device kernel (``dos_coherence_cuda``) reads each subgroup where its
+    state lives: the authoritative working copy in HBM against the fp32
+    params in HBM (static residents: always the whole subgroup, 6 B/param at
+    HBM speed) or in the pinned host pool (everyone else, read over the
+    link: sampled windows, or everything in ``"full"`` mode).  With
+    ``host_io`` the host ``model16`` mirror is checked against the host
+    params the same way.  Host arrays the device cannot read (plain,
+    unregistered numpy memory) are compared on the host instead."""
+    if mode == "off":
+        return
+    torch = __import__("torch")
+    full = mode == "full"
+    lowp = opt.lowp_code
+    w_dev = res.model16
+    esz = w_dev.element_size()
+    ranges, names = [], []
+
+    def add(p_ptr: int, w_ptr: int, n: int, whole: bool, what: str):
+        win = COHERENCE_WINDOW
+        nwin = -(-n // win) if whole else COHERENCE_WINDOWS
+        ranges.append(N.dos_coh_range(p_ptr, w_ptr, n, win, nwin))
+        names.append(what)
+
+    for sg in opt.subgroups:
+        w_ptr = w_dev.data_ptr() + sg.start * esz
+        if sg.index in res.static_sg:
+            add(res.static_sg[sg.index][0].data_ptr(), w_ptr, sg.size, True, f"subgroup {sg.index}")
+        else:
+            add(opt._p.ctypes.data + 4 * sg.start, w_ptr, sg.size, full, f"subgroup {sg.index}")
+            if host_io:
+                add(opt._p.ctypes.data + 4 * sg.start, opt._w.ctypes.data + 2 * sg.start, sg.size, full,
+                    f"subgroup {sg.index} (host model16 mirror)")
+    if not ranges:
+        return
+    arr = (N.dos_coh_range * len(ranges))(*ranges)
+    with torch.cuda.device(res.device):
+        out = torch.tensor([0, -1], dtype=torch.int64, device=res.device)
+        stream = torch.cuda.current_stream(res.device)
+        rc = N.lib().dos_coherence_cuda(arr, len(ranges), lowp,
+                                        C.cast(out.data_ptr(), C.POINTER(C.c_ulonglong)), stream.cuda_stream)
+        if rc == N.DOS_EINVAL and b"device-accessible" in N.lib().dos_last_error():
+            return _coherence_on_host(opt, res, full, host_io)
+        N.check(rc)
+        bad, key = (int(x) for x in out.cpu().tolist())
+    if bad:
+        key &= (1 << 64) - 1
+        r, i = key >> 40, key & ((1 << 40) - 1)
+        raise AssertionError(f"model16 of {names[r]} incoherent with params32 ({bad} elements checked differ, "
+                             f"first at offset {i})")
+
+
+def _coherence_on_host(opt: ShardedOptimizer, res, full: bool, host_io: bool) -> None:
+    torch = __import__("torch")
+    i16 = res.model16.view(torch.int16)
+    for sg in opt.subgroups:
+        if sg.index in res.static_sg:
+            p = res.static_sg[sg.index][0].cpu().numpy()
+            sel = slice(0, sg.size)
+        else:
+            p = opt._p[sg.slice]
+            if full or sg.size <= COHERENCE_WINDOW * COHERENCE_WINDOWS:
+                sel = slice(0, sg.size)
+            else:  # the device kernel's sample: first, last and evenly spread windows
+                starts = [k * (sg.size - COHERENCE_WINDOW) // (COHERENCE_WINDOWS - 1) for k in range(COHERENCE_WINDOWS)]
+                sel = np.concatenate([np.arange(a, a + COHERENCE_WINDOW) for a in starts])
+        want = lowp_downscale(np.ascontiguousarray(p[sel]), opt.lowp).view(np.int16)
+        idx = torch.as_tensor(np.arange(sg.size)[sel] + sg.start, device=res.device)
+        got = i16[idx].cpu().numpy()
+        mirrors = [("", got)]
+        if host_io and sg.index not in res.static_sg:
+            mirrors.append((" (host model16 mirror)", opt._w[sg.slice][sel].view(np.int16)))
+        for tag, have in mirrors:
+            if want.tobytes() != np.ascontiguousarray(have).tobytes():
+                raise AssertionError(f"model16 of subgroup {sg.index}{tag} incoherent with params32")
 
 
 def _pace_replay(timeline: Timeline, scale: float) -> None:

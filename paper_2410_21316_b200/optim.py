@@ -102,19 +102,26 @@ class DeepOptimizerStates:
         opt = ShardedOptimizer.allocate(mine, sg, lowp=self.lowp,
                                         host_homed=[i for i in range(len(sizes)) if i not in static])
         chunk = self.flat[self.offset:self.offset + mine]
-        if master_params is None:
-            p32 = chunk.float()  # exact widening
-        else:
+        m32 = None
+        if master_params is not None:
             flat_m = torch.cat([m.detach().reshape(-1).float().cpu() for m in master_params])
             if flat_m.numel() != total:
                 raise ValueError("master_params must match params element for element")
             m32 = flat_m[self.offset:self.offset + mine].contiguous()
+            del flat_m
             with torch.no_grad():  # working copy = RNE of the masters
                 chunk.copy_(torch.from_numpy(lowp_downscale(m32.numpy(), self.lowp).view(np.int16)).view(dt))
-            p32 = m32.to(dev)
+
+        def masters(a: int, b: int):
+            """fp32 masters of [a, b) of this rank's chunk, widened one range at
+            a time (never the whole shard at once: it is not in the HBM budget)."""
+            return chunk[a:b].float() if m32 is None else m32[a:b]
+
         w16 = chunk.view(torch.int16)
         for a, b in opt.host_runs("state"):
-            torch.from_numpy(opt._p[a:b]).copy_(p32[a:b])
+            for lo in range(a, b, sg):
+                hi = min(b, lo + sg)
+                torch.from_numpy(opt._p[lo:hi]).copy_(masters(lo, hi))
             opt._m[a:b] = 0
             opt._v[a:b] = 0
         for a, b in opt.host_runs("lowp"):
@@ -125,9 +132,11 @@ class DeepOptimizerStates:
         self.res.set_static(static)  # residents start zeroed (m, v) ...
         for i in sorted(static):
             g = opt.subgroups[i]
-            self.res.static_views(i)[0].copy_(p32[g.start:g.stop])  # ... with their masters in HBM
-        del p32
+            self.res.static_views(i)[0].copy_(masters(g.start, g.stop))  # ... with their masters in HBM
+        del m32
         self.coll = BucketedCollectives(lay, process_group) if self.world > 1 else None
+        if master_params is not None and self.coll is not None:
+            self._publish_chunk()  # every rank's copy of the model now holds every rank's new chunk
         # fused all-gather: K1 writes the working copy straight into every
         # peer's full-model buffer (IPC-mapped); else bucketed overlapped gathers
         self.peers = PeerTargets(self.flat, lay, process_group) if (self.world > 1 and fused_gather) else None
@@ -166,6 +175,31 @@ class DeepOptimizerStates:
             raise ValueError("grads are views of the flat HBM buffer; use zero_grad(set_to_none=False)")
         self.flat_grad.zero_()
 
+    def _publish_chunk(self) -> None:
+        """All-gather this rank's chunk of the working copy into every rank's
+        full-model buffer (after it was rewritten outside a phase: init from
+        masters, load_state_dict), then synchronise."""
+        import torch
+
+        lay = self.layout
+        self.coll.all_gather_all(self.flat, self.flat[self.offset:self.offset + lay.per_rank])
+        torch.cuda.current_stream(self.res.device).synchronize()
+        self._barrier()
+
+    def _check_grads_alias_flat(self) -> None:
+        """Grads only reach the optimizer through the flat buffer: a ``.grad``
+        replaced by something else (``zero_grad(set_to_none=True)`` on the
+        model, a user assignment) would be silently ignored — refuse it."""
+        lo = self.flat_grad.data_ptr()
+        hi = lo + self.flat_grad.numel() * self.flat_grad.element_size()
+        for i, p in enumerate(self.params):
+            g = p.grad
+            if g is None or not (lo <= g.data_ptr() < hi):
+                raise RuntimeError(
+                    f"parameter {i}: .grad no longer aliases the optimizer's flat grad buffer "
+                    f"({'None' if g is None else 'a different tensor'}); clear grads with "
+                    f"DeepOptimizerStates.zero_grad() or model.zero_grad(set_to_none=False)")
+
     def _reduce_grads(self) -> None:
         lay = self.layout
         own = self.flat_grad[self.offset:self.offset + lay.per_rank]
@@ -202,6 +236,7 @@ class DeepOptimizerStates:
     def step(self):
         import torch
 
+        self._check_grads_alias_flat()
         torch.cuda.current_stream(self.res.device).synchronize()  # backward done
         gsrc = None
         if self.peer_grads is not None:
@@ -262,3 +297,5 @@ class DeepOptimizerStates:
         for a, b in opt.host_runs("lowp"):
             opt._w[a:b] = w[a:b]
         res.host_stale.discard("_w")
+        if self.coll is not None:
+            self._publish_chunk()  # peers' copies of this chunk were stale until the next step's gather

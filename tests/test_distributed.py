@@ -41,41 +41,76 @@ def test_finalising_actions_cover_every_subgroup():
             assert plan.actions[aid].lane.value != "cpu_compute"
 
 
+def _rank_grads(rank: int, n: int) -> torch.Tensor:
+    """Rank-specific bf16 grads whose sum's rounding depends on the order of
+    the adds: ranks 0 and 2 hold +-x * 2^30 (they cancel), ranks 1 and 3
+    small values that an earlier huge partial sum absorbs."""
+    g = torch.Generator().manual_seed(7)
+    big = torch.randn(n, generator=g) * 2.0 ** 30
+    g = torch.Generator().manual_seed(1000 + rank)
+    small = torch.randn(n, generator=g)
+    x = {0: big, 2: -big}.get(rank % 4, small)
+    return x.to(torch.bfloat16)
+
+
 def _worker(rank, world, port, total, sg, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        from oracle import optistate_oracle as O
+
         lay = ShardLayout.build(total, world, sg)
         coll = BucketedCollectives(lay)
-        # every rank holds full-model grads = (rank + 1) * base
-        base = torch.arange(lay.padded_total, dtype=torch.float32)
-        full = base * (rank + 1)
-        mine = torch.zeros(lay.per_rank)
-        coll.reduce_scatter_all(full, mine)
-        want = base[rank * lay.per_rank:(rank + 1) * lay.per_rank] * sum(r + 1 for r in range(world))
-        ok_rs = torch.equal(mine, want)
+        full = _rank_grads(rank, lay.padded_total)
+        ok_rs = True
+        for scale in (None, 1.0 / world):
+            mine = torch.zeros(lay.per_rank, dtype=torch.bfloat16)
+            coll.reduce_scatter_all(full, mine, scale=scale)
+            lo = rank * lay.per_rank
+            srcs = [_rank_grads(r, lay.padded_total)[lo:lo + lay.per_rank].view(torch.int16).numpy().view(np.uint16)
+                    for r in range(world)]
+            want = O.reduce_scatter(srcs, "bf16", 1.0 if scale is None else scale)
+            ok_rs &= mine.view(torch.int16).numpy().view(np.uint16).tobytes() == want.tobytes()
         # all-gather: each rank contributes rank-tagged params
         shard_params = torch.full((lay.per_rank,), float(rank))
         gathered = torch.full((lay.padded_total,), -1.0)
         coll.all_gather_all(gathered, shard_params)
         want_g = torch.cat([torch.full((lay.per_rank,), float(r)) for r in range(world)])
         q.put((rank, ok_rs, torch.equal(gathered, want_g)))
+    except Exception as e:  # report instead of hanging the parent
+        import traceback
+
+        q.put((rank, traceback.format_exc(), False))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("total,sg", [(1000, 128), (4096, 512)])
-def test_bucketed_collectives_gloo_world2(total, sg):
+@pytest.mark.parametrize("total,sg,world", [(1000, 128, 2), (4096, 512, 2), (5000, 700, 4)])
+def test_bucketed_collectives_gloo(total, sg, world):
+    """Bucketed reduce-scatter = oracle.reduce_scatter (rank-order fp32 sum,
+    one rounding, then the scale) bit for bit, at world 2 and 4; all-gather
+    exact."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, total, sg, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, total, sg, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in procs]
     for p in procs:
         p.join(timeout=60)
-    assert all(ok_rs and ok_ag for _, ok_rs, ok_ag in res), res
+    assert all(ok_rs is True and ok_ag for _, ok_rs, ok_ag in res), res
+
+
+def test_rank_order_reduce_differs_from_other_orders():
+    """The fixture really exercises the order: summing the same four ranks'
+    grads in another order changes some roundings."""
+    from oracle import optistate_oracle as O
+
+    srcs = [_rank_grads(r, 4096).view(torch.int16).numpy().view(np.uint16) for r in range(4)]
+    a = O.reduce_scatter(srcs, "bf16")
+    b = O.reduce_scatter(srcs[::-1], "bf16")
+    assert a.tobytes() != b.tobytes()
 
 
 def _step_worker(rank, world, port, q):

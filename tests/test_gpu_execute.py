@@ -268,3 +268,52 @@ def test_unfused_cpu_downscale_matches(h100, stride):
     opt = D.ShardedOptimizer.initialize(50_000, 5_000, seed=31, lowp="fp16")
     D.execute_plan(opt, D.build_plan(10, stride, 0.2), h100, HYPER, fuse_downscale=False)
     assert digest(opt) == oracle_digest(50_000, 5_000, 31)
+
+
+@pytest.mark.parametrize("host_io", [False, True])
+def test_post_phase_coherence_is_asserted_by_default(h100, host_io):
+    """The reference asserts model16 == downscale_rne(params32) after every
+    phase (executor.py:271-282); so does execute_plan by default: a corrupted
+    working copy of a static resident, of a host-homed subgroup at a sampled
+    window, or (``"full"``) anywhere raises AssertionError."""
+    from paper_2410_21316_b200.executor import COHERENCE_WINDOW, check_coherence_after_phase
+
+    sg = 4 * COHERENCE_WINDOW * 16  # larger than the sample: "sampled" reads a part of each subgroup
+    opt = D.ShardedOptimizer.initialize(6 * sg + 1234, sg, seed=17, lowp="bf16")
+    plan = D.build_plan(7, 2, static_ratio=0.3, placement=Placement.STATIC_FIRST)
+    D.execute_plan(opt, plan, h100, HYPER, host_io=host_io)  # coherent: passes with the default check
+    res = opt.residency
+    static = min(plan.static_set)
+    host = next(i for i in range(7) if i not in plan.static_set)
+    w = res.model16.view(torch.int16)
+    check_coherence_after_phase(opt, res, "full", host_io)
+    for sgi, off, modes in ((static, 12345, ("sampled", "full")),  # residents: always the whole subgroup
+                            (host, 5, ("sampled", "full")),  # first window of a host-homed subgroup
+                            (host, opt.subgroups[host].size - 1, ("sampled", "full")),  # last window
+                            (host, 3 * COHERENCE_WINDOW // 2 + 7, ("full",))):  # between windows
+        i = opt.subgroups[sgi].start + off
+        keep = w[i].clone()
+        w[i] ^= 1
+        for mode in modes:
+            with pytest.raises(AssertionError, match=f"subgroup {sgi}"):
+                check_coherence_after_phase(opt, res, mode, host_io)
+        if modes == ("full",):
+            check_coherence_after_phase(opt, res, "sampled", host_io)
+        w[i] = keep
+    if host_io:  # the host mirror is checked too
+        j = opt.subgroups[host].start + 3
+        opt._w[j] ^= 1
+        with pytest.raises(AssertionError, match="host model16 mirror"):
+            check_coherence_after_phase(opt, res, "sampled", True)
+        opt._w[j] ^= 1
+    check_coherence_after_phase(opt, res, "full", host_io)
+    # the host-side variant (for host arrays the device cannot read) agrees
+    from paper_2410_21316_b200.executor import _coherence_on_host
+
+    _coherence_on_host(opt, res, False, host_io)
+    w[opt.subgroups[host].start] ^= 1
+    with pytest.raises(AssertionError, match=f"subgroup {host}"):
+        _coherence_on_host(opt, res, False, host_io)
+    w[opt.subgroups[host].start] ^= 1
+    with pytest.raises(ValueError):
+        D.execute_plan(opt, plan, h100, HYPER, check_coherence="sometimes")

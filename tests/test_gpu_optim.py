@@ -96,7 +96,14 @@ def test_state_dict_roundtrip_continues_training_exactly(static_ratio):
             opt.step()
         sd = opt.state_dict()
         if load_from is not None:
+            # perturb every tier first: an extra step moves p/m/v and the working
+            # copy, so only a load that restores all of them can match run A
+            opt.zero_grad()
+            model(x).float().pow(2).mean().backward()
+            opt.step()
+            assert opt.state_dict()["momentum32"].tobytes() != load_from["momentum32"].tobytes()
             opt.load_state_dict(load_from)
+            assert opt.step_count == load_from["step"]
         opt.zero_grad()
         model(x).float().pow(2).mean().backward()
         opt.step()
@@ -107,3 +114,17 @@ def test_state_dict_roundtrip_continues_training_exactly(static_ratio):
     assert torch.equal(params_a.view(torch.int16), params_b.view(torch.int16))
     for k in ("params32", "momentum32", "variance32"):
         assert end_a[k].tobytes() == end_b[k].tobytes()
+
+
+def test_replaced_grads_are_refused():
+    """model.zero_grad() (set_to_none=True) detaches .grad from the flat
+    buffer: step() refuses instead of updating with stale grads."""
+    model = _model()
+    opt = DeepOptimizerStates(model.parameters(), subgroup_size=20_000, profile=get_profile("h100-node"), stride=2)
+    x = torch.randn(8, 256, device="cuda", dtype=torch.bfloat16)
+    model(x).float().pow(2).mean().backward()
+    opt.step()
+    model.zero_grad()  # torch 2.x default: set_to_none=True
+    model(x).float().pow(2).mean().backward()
+    with pytest.raises(RuntimeError, match="no longer aliases"):
+        opt.step()

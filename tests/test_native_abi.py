@@ -159,3 +159,39 @@ def test_pinned_pool_alloc_roundtrip():
     a[:] = np.arange(1000, dtype=np.float32)
     assert a.sum() == np.arange(1000, dtype=np.float32).sum()
     assert a.ctypes.data % 4096 == 0
+
+
+def test_team_resize_while_h1_runs():
+    """dos_set_host_threads while another thread is inside an H1 section:
+    the running section keeps its team (no use-after-free) and every result
+    stays bit-exact (dos_host.cpp team lifetime)."""
+    import threading
+
+    n = 1 << 20
+    rng = np.random.default_rng(5)
+    p0, m0, g = (rng.normal(0, s, n).astype(np.float32) for s in (0.02, 1e-3, 1.0))
+    v0 = (rng.random(n) * 1e-4).astype(np.float32)
+    want = [x.copy() for x in (p0, m0, v0)]
+    O.adam_step(*want, g, 1e-3, 0.9, 0.999, 1e-8, 1)
+    errors, stop = [], threading.Event()
+
+    def work():
+        try:
+            while not stop.is_set():
+                p, m, v = p0.copy(), m0.copy(), v0.copy()
+                D.adam_step_arrays(p, m, v, g, 1e-3, 0.9, 0.999, 1e-8, 1)
+                if p.tobytes() != want[0].tobytes() or v.tobytes() != want[2].tobytes():
+                    errors.append("mismatch")
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(repr(e))
+
+    th = threading.Thread(target=work)
+    th.start()
+    try:
+        for i in range(40):
+            N.check(N.lib().dos_set_host_threads(1 + i % 4))
+    finally:
+        stop.set()
+        th.join(timeout=120)
+    N.check(N.lib().dos_set_host_threads(0))
+    assert not th.is_alive() and not errors, errors
