@@ -6,7 +6,9 @@ Workload at N=1: BASELINE.json configs[1] — a 7B-param (Llama-2-7B-sized)
 optimizer shard, fp32 Adam with bf16 grads and a bf16 working copy, 1e8-param
 subgroups, fp32 p/m/v homed in pinned host memory (host offload), the
 CPU/GPU interleave stride chosen by the performance model from constants
-measured on this box.  A step is one full update phase over the shard.
+measured on this box.  A step is one full update phase over the shard as an
+iteration runs it: the CPU-updated subgroups' bf16 grads flushed D2H inside
+the phase, the reference's post-phase coherence assertion on.
 Synthetic, seeded data generated on the device (no dataset exists).
 
 Under torchrun (N>1) the same 7B shard is ZeRO-3 partitioned across ranks
@@ -62,6 +64,9 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=70,
                     help="1e8-param subgroups timed for the cpu_baseline (70 = one full 7B phase, ~25 core-seconds)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-grad-flush", action="store_true",
+                    help="time the phase with the CPU subgroups' grads pre-staged on the host (the headline "
+                         "includes their in-phase D2H flush by default)")
     ap.add_argument("--host-threads", type=int, default=0, help="H1 team size (0: all allowed cores / ranks)")
     ap.add_argument("--trace-dir", default=None, help="write measured/predicted timelines as trace CSVs")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -191,23 +196,153 @@ def host_available_bytes() -> int:
     return 1 << 62
 
 
-def cpu_oracle_rate(sg: int, nsub: int, lowp: str, threads: int) -> dict:
-    """The oracle port (C restatement of the reference loop) on host cores."""
+class CpuShard:
+    """Host state for the CPU reference path: ``nbuf`` distinct subgroup
+    buffers of ``sg`` params (p, m, v fp32, grads and working copy 16-bit),
+    the reference's value distributions (core.py:259-272) drawn once and
+    replicated.  ``nbuf`` = the shard's subgroup count streams the whole
+    shard through host DRAM each step, like the B200 arm's pinned pool."""
+
+    def __init__(self, sg: int, nbuf: int) -> None:
+        rng = np.random.default_rng(0)
+        p = (rng.standard_normal(sg, dtype=np.float32) * np.float32(0.02))
+        m = (rng.standard_normal(sg, dtype=np.float32) * np.float32(1e-3))
+        v = rng.random(sg, dtype=np.float32) * np.float32(1e-4)
+        g = (rng.standard_normal(sg, dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
+        self.bufs = []
+        for i in range(nbuf):
+            self.bufs.append((p.copy(), m.copy(), v.copy(), g if i == 0 else g.copy(), np.empty(sg, dtype=np.uint16)))
+        self.sg = sg
+
+
+def cpu_oracle_rate(sg: int, nsub: int, lowp: str, threads: int, shard: CpuShard | None = None,
+                    step: int = 2) -> dict:
+    """The oracle port (C restatement of the reference loop, threaded) over
+    ``nsub`` subgroup passes: across ``shard``'s distinct buffers, or one
+    reused buffer when no shard is given."""
     from oracle import c_oracle
 
     c_oracle.build()
-    rng = np.random.default_rng(0)
-    p = (rng.standard_normal(sg, dtype=np.float32) * np.float32(0.02))
-    m = (rng.standard_normal(sg, dtype=np.float32) * np.float32(1e-3))
-    v = rng.random(sg, dtype=np.float32) * np.float32(1e-4)
-    g = (rng.standard_normal(sg, dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
-    w = np.empty(sg, dtype=np.uint16)
-    c_oracle.adam_mt(p, m, v, g, lowp, w, lowp, 1e-3, 0.9, 0.999, 1e-8, 1, nthreads=threads)  # warm
+    shard = shard or CpuShard(sg, 1)
+    c_oracle.adam_mt(*shard.bufs[0][:4], lowp, shard.bufs[0][4], lowp, 1e-3, 0.9, 0.999, 1e-8, 1,
+                     nthreads=threads)  # warm
     t0 = time.perf_counter()
     for s in range(nsub):
-        c_oracle.adam_mt(p, m, v, g, lowp, w, lowp, 1e-3, 0.9, 0.999, 1e-8, 2 + s, nthreads=threads)
+        p, m, v, g, w = shard.bufs[s % len(shard.bufs)]
+        c_oracle.adam_mt(p, m, v, g, lowp, w, lowp, 1e-3, 0.9, 0.999, 1e-8, step, nthreads=threads)
     dt = time.perf_counter() - t0
     return {"value": nsub * sg / dt, "seconds": dt, "params": nsub * sg}
+
+
+def host_facts(gpu_index: int | None = None) -> dict:
+    """The host the line was measured on (lscpu + NUMA)."""
+    out: dict = {"logical_cpus": os.cpu_count(), "affinity_cpus": len(os.sched_getaffinity(0))}
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                out["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        out["lscpu"] = {k.strip(): v.strip() for k, v in (ln.split(":", 1) for ln in subprocess.run(
+            ["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines() if ":" in ln)
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core", "NUMA node(s)",
+                             "L3 cache", "CPU max MHz", "Hypervisor vendor")}
+    except Exception:
+        pass
+    nodes = {}
+    base = Path("/sys/devices/system/node")
+    for d in sorted(base.glob("node[0-9]*")) if base.exists() else []:
+        try:
+            nodes[d.name] = (d / "cpulist").read_text().strip()
+        except OSError:
+            pass
+    out["numa_nodes"] = nodes
+    out["mem_total_gb"] = round(host_total_bytes() / 2**30, 1)
+    try:
+        out["thp"] = Path("/sys/kernel/mm/transparent_hugepage/enabled").read_text().strip()
+    except OSError:
+        pass
+    if gpu_index is not None:
+        try:
+            from paper_2410_21316_b200.distributed import gpu_numa_node
+
+            out["gpu_numa_node"] = gpu_numa_node(gpu_index)
+        except Exception:
+            pass
+    return out
+
+
+def host_total_bytes() -> int:
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def joint_bound(host_homed: int, static: int, hbm_Bps: float, link_Bps: float, dram_Bps: float,
+                h1_params_per_s: float, flush: bool, grid: int = 2000) -> dict:
+    """Plan-independent lower bound on the phase for this residency: over
+    every split of the ``host_homed`` params into a streamed fraction x
+    (through the B200: 12 B each way over the link, 24 B of host DRAM) and a
+    host-updated rest (2 B H2D of its working copy, + 2 B D2H of its grads
+    with the in-phase flush; 30/32 B of host DRAM; H1 at its best measured
+    rate), the slowest resource's time, minimised over x (a continuous
+    relaxation of the strides, so no plan can beat it)."""
+    D, best = float(host_homed), None
+    gB = 2.0 if flush else 0.0
+    for i in range(grid + 1):
+        x = i / grid
+        t = {"hbm": BYTES_PER_PARAM_K1 * (static + x * D) / hbm_Bps,
+             "link": max((12 * x + 2 * (1 - x)) * D, (12 * x + gB * (1 - x)) * D) / link_Bps,
+             "host_dram": (24 * x + (30 + gB) * (1 - x)) * D / dram_Bps if dram_Bps else 0.0,
+             "host_compute": (1 - x) * D / h1_params_per_s if h1_params_per_s else 0.0}
+        k = max(t, key=t.get)
+        if best is None or t[k] < best[0]:
+            best = (t[k], x, k, t)
+    return {"ideal_ms": best[0] * 1e3, "streamed_fraction": best[1], "binding": best[2],
+            "bounds_ms_at_optimum": {k: v * 1e3 for k, v in best[3].items()}}
+
+
+REF_INSTALL = ROOT / "baseline" / "_ref"
+
+
+def reference_1core_rate(sg: int, nsub: int = 2) -> dict:
+    """The literal reference CPU path: the
+    unmodified reference's ``sequential_oracle`` (executor.py:103-117: numba
+    ``_adam_step_jit`` kernels.py:88-101 per subgroup + numpy fp16 up/down
+    casts, one thread under the GIL), from the copy installed in
+    ``baseline/_ref`` (tools/install_reference.sh), timed on ``nsub``
+    subgroups of ``sg`` params with the reference's value distributions."""
+    if not (REF_INSTALL / "optistate").exists():
+        return {"unavailable": "reference not installed in baseline/_ref (tools/install_reference.sh)"}
+    if str(REF_INSTALL) not in sys.path:
+        sys.path.insert(0, str(REF_INSTALL))
+    try:
+        import optistate as R
+    except Exception as exc:  # e.g. numba missing on this host
+        return {"unavailable": f"reference import failed: {exc!r}"[:200]}
+    backend = R.kernels.active_backend()
+    warm = R.ShardedOptimizer.initialize(4096, 1024, seed=0)  # numba compile outside the timing
+    R.sequential_oracle(warm, R.AdamHyper())
+    n = sg * nsub
+    rng = np.random.default_rng(0)
+    p = (rng.standard_normal(n, dtype=np.float32) * np.float32(0.02))
+    opt = R.ShardedOptimizer(subgroups=R.shard(n, 1, sg)[0], params32=p,
+                             momentum32=rng.standard_normal(n, dtype=np.float32) * np.float32(1e-3),
+                             variance32=rng.random(n, dtype=np.float32) * np.float32(1e-4),
+                             model16=p.astype(np.float16),
+                             grads16=rng.standard_normal(n, dtype=np.float32).astype(np.float16))
+    t0 = time.perf_counter()
+    R.sequential_oracle(opt, R.AdamHyper())
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "reference", "backend": backend,
+            "seconds": dt, "sample": f"reference sequential_oracle (baseline/_ref, {backend}) over {nsub} x "
+                                     f"{sg:.0e}-param subgroups, fp16 grads/model16, 1 thread"}
 
 
 # ---------------------------------------------------------------- reference arm
@@ -218,21 +353,31 @@ def run_reference(args, rank: int, world: int) -> None:
         return
     threads = len(os.sched_getaffinity(0))
     sg = int(args.subgroup)
-    # one step = the whole phase's work (P/SG subgroup passes, each over a
-    # resident 1e8-param buffer far larger than the LLC)
+    # one step = the whole phase's work: P/SG subgroup passes, over the whole
+    # shard's distinct host buffers (16 B/param) when they fit in host RAM —
+    # like-for-like with the B200 arm's pinned pool — else over as many
+    # distinct 1e8-param buffers as fit (each far larger than the LLC)
     nsub = max(1, math.ceil(args.params / args.subgroup))
-    for _ in range(args.warmup):  # untimed full steps
-        cpu_oracle_rate(sg, nsub, args.lowp, threads)
+    fit = int((host_available_bytes() - (16 << 30)) // (16 * sg))
+    nbuf = max(1, min(nsub, fit))
+    t0 = time.perf_counter()
+    shard = CpuShard(sg, nbuf)
+    fill_s = time.perf_counter() - t0
+    for w in range(args.warmup):  # untimed full steps
+        cpu_oracle_rate(sg, nsub, args.lowp, threads, shard, step=1 + w)
     vals, secs = [], 0.0
-    for _ in range(args.steps):
-        r = cpu_oracle_rate(sg, nsub, args.lowp, threads)
+    for k in range(args.steps):
+        r = cpu_oracle_rate(sg, nsub, args.lowp, threads, shard, step=1 + args.warmup + k)
         vals.append(r["value"])
         secs += r["seconds"]
     value = float(np.median(vals))
-    one = cpu_oracle_rate(sg, 2, args.lowp, 1)  # context: the reference's single-threaded loop
+    del shard
+    one = cpu_oracle_rate(sg, 2, args.lowp, 1)  # context: the port's single-threaded loop
+    ref1 = reference_1core_rate(sg, 2)
     P = int(args.params)
     sample = (f"{nsub} x {sg:.0e}-param subgroup passes per step = the full {P / 1e9:g}B phase "
-              f"(Adam + {args.lowp} working copy, sequential_oracle order), reusing one resident subgroup buffer")
+              f"(Adam + {args.lowp} working copy, sequential_oracle order) over {nbuf} distinct subgroup "
+              f"buffers ({16 * sg * nbuf / 1e9:.0f} GB of host state)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
@@ -241,9 +386,11 @@ def run_reference(args, rank: int, world: int) -> None:
         "config": {"workload": f"{P / 1e9:g}B-param Adam shard, {args.lowp} grads, sg={sg:.0e}, host cores only",
                    "params": P, "subgroup": sg},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
-                         "single_thread_value": one["value"]},
+                         "single_thread_value": one["value"], "distinct_buffers": nbuf, "fill_s": fill_s,
+                         "ref_1core": ref1},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
+        "host": host_facts(),
     }
     print(json.dumps(line), flush=True)
 
@@ -321,6 +468,14 @@ class B200Bench:
         torch.cuda.synchronize()
         return self.max_over_ranks(e0.elapsed_time(e1) / steps)
 
+    def phase(self, plan, **kw):
+        """One update phase as an iteration runs it: the host lane's grads
+        flushed D2H inside the phase (the D2H of the CPU
+        subgroups' grads is part of the iteration), the reference's
+        post-phase coherence assertion on (sampled; executor.py:271-282)."""
+        kw.setdefault("flush_grads", not self.args.no_grad_flush)
+        return self.D.execute_plan(self.opt, plan, self.profile, self.hyper, **kw)
+
     # -- phases of the run
     def cpu_baseline(self) -> None:
         """The oracle port on the host cores, before the pinned shard exists (rank 0, N=1)."""
@@ -332,8 +487,11 @@ class B200Bench:
         r = cpu_oracle_rate(self.SG, a.cpu_sample, a.lowp, threads)
         self.out["cpu_baseline"] = {
             "value": r["value"], "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{a.cpu_sample} x {a.subgroup:.0e}-param subgroups ({r['seconds']:.1f} s), "
-                      f"oracle/adam_oracle.c (reference loop restated) with {threads} threads"}
+            "sample": f"{a.cpu_sample} x {a.subgroup:.0e}-param subgroup passes over one reused buffer "
+                      f"({r['seconds']:.1f} s), oracle/adam_oracle.c (reference loop restated) with {threads} "
+                      f"threads; --impl reference streams the whole shard's distinct buffers",
+            # the literal reference code path, single-threaded
+            "ref_1core": reference_1core_rate(self.SG, 2)}
 
     def setup(self) -> None:
         D, a, torch = self.D, self.args, self.torch
@@ -351,6 +509,9 @@ class B200Bench:
             self.static_ratio = float(a.static_ratio)
         self.placement = D.Placement(a.placement)
         static = D.build_plan(self.nsg, 1, static_ratio=self.static_ratio, placement=self.placement).static_set
+        # the link's peak, probed on a quiet box with buffers allocated before
+        # the pool (and reused by the later re-probe, copy_streams)
+        self.link_setup = self.profile_b200.measure_link(1 << 30, numa_node=self.numa)
         t0 = time.perf_counter()
         # sparse pinned pool: host memory only for the host-homed subgroups
         self.opt = D.ShardedOptimizer.allocate(self.P_rank, self.SG, lowp=a.lowp, numa_node=self.numa,
@@ -380,7 +541,7 @@ class B200Bench:
             stride = int(a.stride)
         self.plan = D.build_plan(self.nsg, stride, static_ratio=self.static_ratio, placement=self.placement)
         if a.stride == "auto":
-            r = D.execute_plan(self.opt, self.plan, self.profile, self.hyper)
+            r = self.phase(self.plan)
             self.profile = self.broadcast(self.policy.refit_profile(self.profile, r.measured, self.sizes))
             tuner = self.tune(self.static_ratio, explore=4)
             self.stride_spans = tuner.predicted
@@ -405,7 +566,7 @@ class B200Bench:
         tuner.queue = list(self.broadcast(tuner.queue))  # same exploration order on every rank
         while tuner.exploring:
             k = tuner.next_stride()
-            r = D.execute_plan(self.opt, tuner.plan_for(k), self.profile, self.hyper)
+            r = self.phase(tuner.plan_for(k))
             tuner.record(k, self.max_over_ranks(r.measured.span_ns))
         return tuner
 
@@ -413,7 +574,7 @@ class B200Bench:
         """W warm-up steps, then exactly K timed steps (device-resident grads)."""
         torch, D, a = self.torch, self.D, self.args
         for _ in range(a.warmup):
-            D.execute_plan(self.opt, self.plan, self.profile, self.hyper)
+            self.phase(self.plan)
         clocks = ClockSampler(self.device.index)
         self.barrier()
         torch.cuda.synchronize()
@@ -424,7 +585,7 @@ class B200Bench:
         torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include timed/ captures exactly this region
         e0.record()
         for _ in range(a.steps):
-            self.results.append(D.execute_plan(self.opt, self.plan, self.profile, self.hyper))
+            self.results.append(self.phase(self.plan))
         e1.record()
         torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
@@ -467,42 +628,62 @@ class B200Bench:
         self.out["roofline"]["standalone"] = {"achieved": alone["k1_GBs"], "frac": alone["k1_GBs"] / hbm_peak,
                                               "ms_per_launch": alone["k1_ms"], "params": alone["n"]}
         # phase: HBM time of the fast-tier params, busier link direction at the
-        # measured per-direction rate, host DRAM (24 B per streamed param of DMA,
-        # 28 B per host-updated param of H1 + 2 B read by its H2D_PARAMS16) at the
-        # rate measured for H1 + duplex DMA sharing the host memory
+        # measured per-direction rate, host DRAM (24 B per streamed param of DMA;
+        # 28 B per host-updated param of H1 + 2 B read by its H2D_PARAMS16 + 2 B
+        # written by its in-phase grad flush) at the best host-memory rate
+        # measured in this run
         prof = self.profile
+        flush = not self.args.no_grad_flush
         fast = sum(self.sizes[i] for i, d in enumerate(plan.devices) if d is D.Device.FAST)
         static = sum(self.sizes[i] for i in plan.static_set)
         cpu = self.P_rank - fast
-        host_bytes = 24 * (fast - static) + 30 * cpu
-        link_Bps = prof.channel_params_per_s * 4.0
+        self.grads_d2h_b = 2 * cpu if flush else 0
+        cpu_host_B = 30 + (2 if flush else 0)
+        host_bytes = 24 * (fast - static) + cpu_host_B * cpu
+        raw = self.profile_b200.LAST_RAW
+        # the link's peak per direction: the best duplex probe of this run
+        link_Bps = max(self.link_setup["duplex_GBs_per_dir"], raw.get("link", {}).get("duplex_GBs_per_dir", 0.0)) * 1e9
         # host DRAM peak: the best of the team's read / copy passes (alone and
         # with duplex DMA) and H1 + duplex DMA, all measured in this run
-        raw = self.profile_b200.LAST_RAW
         dram_probe = raw.get("host_dram", {})
         dram_Bps = max(dram_probe.get("peak_GBs", 0.0), raw.get("h1_with_dma", {}).get("host_dram_GBs_combined", 0.0),
                        raw.get("h1_alone", {}).get("h1_GBs", 0.0)) * 1e9
+        h1_rate = raw.get("h1_alone", {}).get("h1_params_per_s", prof.cpu_update_params_per_s)
+        link_dir_b = max(self.h2d_b, self.d2h_b + self.grads_d2h_b)
         bounds = {"hbm": BYTES_PER_PARAM_K1 * fast / (hbm_peak * 1e9),
-                  "link": max(self.h2d_b, self.d2h_b) / link_Bps,
+                  "link": link_dir_b / link_Bps,
                   "host_dram": host_bytes / dram_Bps if dram_Bps else 0.0}
         bound = max(bounds, key=bounds.get)
+        joint = joint_bound(self.P_rank - static, static, hbm_peak * 1e9, link_Bps, dram_Bps, h1_rate, flush)
+        ns = max(bounds["hbm"], bounds["link"])
         self.out["phase_roofline"] = {
             "bound": bound, "ideal_ms": bounds[bound] * 1e3, "achieved_ms": self.ms,
             "frac": bounds[bound] * 1e3 / self.ms, "bounds_ms": {k: v * 1e3 for k, v in bounds.items()},
+            "note": "plan-dependent: the bytes of the chosen split; joint_bound is the plan-independent one",
+            "joint_bound": {**joint, "frac": joint["ideal_ms"] / self.ms},
+            # north_star's roofline: the slower of 28 B/param at HBM peak and the
+            # offloaded bytes (this plan's busier link direction) at the link peak
+            "north_star": {"ideal_ms": ns * 1e3, "frac": ns * 1e3 / self.ms,
+                           "bound": "link" if bounds["link"] >= bounds["hbm"] else "hbm"},
             "link_GBs_per_dir_measured": link_Bps / 1e9, "host_dram_bytes_per_step": host_bytes,
+            "host_dram_bytes_per_param": {"streamed": 24, "host_updated": cpu_host_B},
             "host_dram_GBs_measured": dram_Bps / 1e9, "host_dram_probe": dram_probe,
-            "host_update_ms_at_measured_rate": cpu / prof.cpu_update_params_per_s * 1e3}
+            "host_update_ms_at_measured_rate": cpu / prof.cpu_update_params_per_s * 1e3,
+            "grad_flush_in_phase": flush}
         spans = [r.measured.span_ns for r in self.results]
         self.out["iteration"] = {
             "update_span_ms_median": float(np.median(spans)) / 1e6,
             "update_makespan_ms_median": float(np.median([r.measured.makespan_ns for r in self.results])) / 1e6,
             "predicted_makespan_ms": pred.makespan_ns / 1e6, "predicted_span_ms": pred.span_ns / 1e6,
             "lane_busy_ms_per_step": {k: v / 1e6 / len(self.results) for k, v in lane_busy.items()},
-            "h2d_bytes_per_step": self.h2d_b, "d2h_bytes_per_step": self.d2h_b}
+            "h2d_bytes_per_step": self.h2d_b, "d2h_bytes_per_step": self.d2h_b + self.grads_d2h_b}
 
     def grad_flush(self) -> None:
-        """§8(f) row 1: the host lane needs the host subgroups' grads — flushed
-        D2H before the phase, and alternatively inside it (flush_grads)."""
+        """§8(f) row 1: the host lane needs the host subgroups' grads.  The
+        headline flushes them inside the phase (``flush_grads``); for context,
+        the same phase with them flushed before it (a separate D2H pass, then
+        the phase on pre-staged grads), and the cost of the default post-phase
+        coherence assertion."""
         torch, D, opt = self.torch, self.D, self.opt
         cpu_sgs = [g for i, g in enumerate(opt.subgroups) if self.plan.devices[i] is D.Device.CPU]
         dev_g16 = opt.residency.grads.view(torch.int16)
@@ -513,15 +694,26 @@ class B200Bench:
                 host_g16[g.start:g.stop].copy_(dev_g16[g.start:g.stop], non_blocking=True)
 
         flush_ms = self.timed(flush, 1)
-        D.execute_plan(opt, self.plan, self.profile, self.hyper, flush_grads=True)
-        in_phase = self.timed(lambda: D.execute_plan(opt, self.plan, self.profile, self.hyper, flush_grads=True),
-                              self.args.steps)
+        self.phase(self.plan, flush_grads=False)
+        staged = self.timed(lambda: self.phase(self.plan, flush_grads=False), self.args.steps)
+        from paper_2410_21316_b200.executor import check_coherence_after_phase
+
+        coh = {}
+        for mode in ("sampled", "full"):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            check_coherence_after_phase(opt, opt.residency, mode)
+            coh[f"{mode}_ms"] = (time.perf_counter() - t0) * 1e3
+        coh["sampled_frac_of_phase"] = coh["sampled_ms"] / self.ms
+        with_flush = not self.args.no_grad_flush
         self.out["iteration"].update({
             "grad_flush_ms": flush_ms, "grad_flush_bytes": 2 * sum(g.size for g in cpu_sgs),
-            "phase_with_in_phase_grad_flush_ms": in_phase,
-            # the update part of an iteration: grad flush + phase (+ RS at N>1; the
-            # all-gather is overlapped or fused), flush before or inside the phase
-            "iteration_update_ms": min(flush_ms + self.ms, in_phase)})
+            "phase_with_in_phase_grad_flush_ms": self.ms if with_flush else None,
+            "phase_on_prestaged_grads_ms": staged,
+            # the update part of an iteration at N=1: grad flush + phase, the
+            # flush before or inside the phase (+ RS/AG at N>1, see collectives)
+            "iteration_update_ms": min(flush_ms + staged, self.ms) if with_flush else flush_ms + self.ms,
+            "coherence_check": coh})
 
     def e2e(self) -> None:
         """Through the public API with host buffers: grads read from pinned
@@ -583,7 +775,7 @@ class B200Bench:
 
         def overlapped():
             hook = gather_params_overlapped(coll, self.plan, self.opt.residency.model16, full)
-            D.execute_plan(self.opt, self.plan, self.profile, self.hyper, on_submitted=hook)
+            self.phase(self.plan, on_submitted=hook)
             for w in hook.works:
                 if w is not None:
                     w.wait()
@@ -599,7 +791,7 @@ class B200Bench:
         # every rank must agree before anyone waits in the fused phase's barrier
         if -self.max_over_ranks(-1.0 if pgrads is not None else 0.0) >= 1.0:
             def fused():
-                D.execute_plan(self.opt, self.plan, self.profile, self.hyper, peers=peers.targets)
+                self.phase(self.plan, peers=peers.targets)
                 peers.barrier()
 
             fused_ms = self.timed(fused, 1)
@@ -612,8 +804,7 @@ class B200Bench:
 
             def fused_all():
                 self.barrier()
-                D.execute_plan(self.opt, self.plan, self.profile, self.hyper, peers=peers.targets, flush_grads=True,
-                               grad_sources=gsrc)
+                self.phase(self.plan, peers=peers.targets, flush_grads=True, grad_sources=gsrc)
                 self.barrier()
 
             fused_all_ms = self.timed(fused_all, 1)
@@ -642,8 +833,8 @@ class B200Bench:
                 continue
             tuner = self.tune(ratio, explore=3)  # untimed; the first step also moves the residents
             vplan = tuner.plan()
-            D.execute_plan(self.opt, vplan, self.profile, self.hyper)
-            ms = self.timed(lambda: D.execute_plan(self.opt, vplan, self.profile, self.hyper), self.args.steps)
+            self.phase(vplan)
+            ms = self.timed(lambda: self.phase(vplan), self.args.steps)
             variants.append({"static_ratio": ratio, "stride": vplan.stride, "ms_per_step": ms,
                              "value": self.P / (ms * 1e-3),
                              "hbm_resident_state_bytes": 12 * sum(self.sizes[i] for i in vplan.static_set) * self.world})
@@ -663,12 +854,13 @@ class B200Bench:
         if not self.host_fits(0.0):
             self.out["copy_streams"] = {"skipped": "the whole shard would not fit in pinned host memory"}
             return
-        link = self.profile_b200.measure_link(1 << 30)
+        # re-probe on the setup's buffers; the denominator is the best duplex
+        # rate of every probe in this run (a lower late probe must not flatter frac)
+        link = self.profile_b200.measure_link(1 << 30, numa_node=self.numa)
         splan = D.build_plan(self.nsg, 1, static_ratio=0.0)
-        D.execute_plan(self.opt, splan, self.profile, self.hyper)  # moves any residents home
+        self.phase(splan)  # moves any residents home
         res: list = []
-        ms = self.timed(lambda: res.append(D.execute_plan(self.opt, splan, self.profile, self.hyper)),
-                        self.args.steps)
+        ms = self.timed(lambda: res.append(self.phase(splan)), self.args.steps)
         ev = res[-1].timeline.events
         h2d_b = sum(e.bytes for e in ev if e.action.lane.value == "h2d")
         d2h_b = sum(e.bytes for e in ev if e.action.lane.value == "d2h")
@@ -687,14 +879,20 @@ class B200Bench:
         spans = [r.measured.span_ns for r in res]
         link_ns = [union_ns(r, ("h2d", "d2h")) for r in res]
         k1_ns = [sum(e.duration_ns for e in r.measured.events if e.action.lane.value == "fast_compute") for r in res]
-        duplex = link["duplex_GBs_per_dir"]
+        probes = {"setup": self.link_setup, "now": link,
+                  "profile": self.profile_b200.LAST_RAW.get("link", {})}
+        duplex = max(p.get("duplex_GBs_per_dir", 0.0) for p in probes.values())
         per_dir = {"h2d": h2d_b / (ms * 1e-3) / 1e9, "d2h": d2h_b / (ms * 1e-3) / 1e9}
+        frac = min(per_dir.values()) / duplex
         self.out["copy_streams"] = {
             "plan": "stride 1, static_ratio 0 (every subgroup streamed through the B200)",
             "ms_per_step": ms, "value": self.P / (ms * 1e-3),
             "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
-            "achieved_GBs_per_dir": per_dir, "link_measured_GBs": link,
-            "frac": min(per_dir.values()) / duplex, "peak": duplex, "peak_source": "duplex pinned copy, measured here",
+            "achieved_GBs_per_dir": per_dir, "link_probes_GBs": probes,
+            # a fraction above 1.05 means the probe under-measured the link: no number
+            "frac": frac if frac <= 1.05 else None,
+            "error": None if frac <= 1.05 else f"achieved {frac:.3f} of the best probe: the link probe is wrong",
+            "peak": duplex, "peak_source": "best duplex pinned copy of this run's probes (1 GiB each way, best of 3)",
             # K1 runs while the link is busy: the time the link sits idle inside
             # the span is the update's exposed part (pipeline fill + drain included)
             "update_busy_ms": float(np.median(k1_ns)) / 1e6,
@@ -712,8 +910,8 @@ class B200Bench:
             self.out["reference_offload_schedule"] = {"skipped": "the whole shard would not fit in pinned host memory"}
             return
         rplan = D.build_plan(self.nsg, D.ALL_CPU)
-        D.execute_plan(self.opt, rplan, self.profile, self.hyper)
-        ms = self.timed(lambda: D.execute_plan(self.opt, rplan, self.profile, self.hyper), 2)
+        self.phase(rplan)
+        ms = self.timed(lambda: self.phase(rplan), 2)
         self.out["reference_offload_schedule"] = {
             "ms_per_step": ms, "value": self.P / (ms * 1e-3), "speedup_of_headline": ms / self.ms,
             "plan": "build_plan(N, ALL_CPU): CPU_UPDATE -> CPU_DOWNSCALE -> H2D_PARAMS16 chained"}
@@ -761,6 +959,7 @@ class B200Bench:
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic (seeded, generated on device)", "config": config}
         line.update(self.out)
+        line["host"] = host_facts(self.device.index)
         line["profile"] = {"channel_params_per_s": prof.channel_params_per_s,
                            "fast_update_params_per_s": prof.fast_update_params_per_s,
                            "cpu_update_params_per_s": prof.cpu_update_params_per_s,

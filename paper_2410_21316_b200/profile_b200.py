@@ -40,17 +40,31 @@ def _torch():
     return torch
 
 
-def measure_link(nbytes: int = 1 << 30, reps: int = 3) -> dict:
-    """Pinned host<->device GB/s: each direction alone and both at once."""
+_LINK_BUFS: dict = {}  # nbytes -> probe buffers, allocated once per process and reused
+
+
+def _link_buffers(nbytes: int, numa_node: int = -1):
+    """Pinned probe buffers of ``nbytes`` (pre-faulted huge pages, registered)
+    and their device twins, allocated on first use and kept: a probe late in a
+    run reuses the pages it got at start-up instead of fresh ones from a
+    fragmented host (which measured the link 30-40% low in round 1)."""
     torch = _torch()
-    dev = torch.device("cuda")
-    hb1 = N.HostBuffer(nbytes)
-    hb2 = N.HostBuffer(nbytes)
-    h1 = torch.from_numpy(hb1.array(np.uint8, nbytes))
-    h2 = torch.from_numpy(hb2.array(np.uint8, nbytes))
-    d1 = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-    d2 = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    key = (nbytes, numa_node, torch.cuda.current_device())
+    if key not in _LINK_BUFS:
+        hb1, hb2 = N.HostBuffer(nbytes, numa_node=numa_node), N.HostBuffer(nbytes, numa_node=numa_node)
+        h1 = torch.from_numpy(hb1.array(np.uint8, nbytes))
+        h2 = torch.from_numpy(hb2.array(np.uint8, nbytes))
+        d1 = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        d2 = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        _LINK_BUFS[key] = (hb1, hb2, h1, h2, d1, d2, torch.cuda.Stream(), torch.cuda.Stream())
+    return _LINK_BUFS[key]
+
+
+def measure_link(nbytes: int = 1 << 30, reps: int = 3, numa_node: int = -1) -> dict:
+    """Pinned host<->device GB/s: each direction alone and both at once
+    (best of ``reps``; buffers reused across calls, see ``_link_buffers``)."""
+    torch = _torch()
+    _, _, h1, h2, d1, d2, s1, s2 = _link_buffers(nbytes, numa_node)
 
     def timed(fn) -> float:
         fn()
