@@ -63,6 +63,11 @@ def parse():
                     help="imposed dynamic fast-tier budget (default: two windows)")
     ap.add_argument("--cpu-sample", type=int, default=70,
                     help="1e8-param subgroups timed for the cpu_baseline (70 = one full 7B phase, ~25 core-seconds)")
+    ap.add_argument("--configs", default=None,
+                    help="comma-separated BASELINE configs to run after the headline (13B/2,20B/4,20B/8,70B/8); "
+                         "default: the ones matching --gpus (2: 13B/2, 4: 20B/4, 8: 20B/8 + the 70B/8 sweep)")
+    ap.add_argument("--config-scale", type=float, default=1.0, help="scale the configs' parameter counts (dry runs)")
+    ap.add_argument("--config-steps", type=int, default=3, help="timed steps per config variant")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-grad-flush", action="store_true",
                     help="time the phase with the CPU subgroups' grads pre-staged on the host (the headline "
@@ -418,6 +423,7 @@ class B200Bench:
         self.device = torch.device("cuda", dev_index)
         if world > 1:
             if args.dist_backend == "nccl":
+                os.environ.setdefault("NCCL_DEBUG", "INFO")  # the log shows every rank joining
                 dist.init_process_group("nccl", device_id=self.device)
             else:
                 dist.init_process_group("gloo")
@@ -474,7 +480,8 @@ class B200Bench:
         subgroups' grads is part of the iteration), the reference's
         post-phase coherence assertion on (sampled; executor.py:271-282)."""
         kw.setdefault("flush_grads", not self.args.no_grad_flush)
-        return self.D.execute_plan(self.opt, plan, self.profile, self.hyper, **kw)
+        opt = kw.pop("opt", None) or self.opt
+        return self.D.execute_plan(opt, plan, self.profile, self.hyper, **kw)
 
     # -- phases of the run
     def cpu_baseline(self) -> None:
@@ -554,19 +561,26 @@ class B200Bench:
         pinned) fit in the host memory still available?"""
         static = self.D.build_plan(self.nsg, 1, static_ratio=ratio, placement=self.placement).static_set
         need = 16 * sum(s for i, s in enumerate(self.sizes) if i not in static)
-        ok = need <= self.opt.host_bytes + host_available_bytes() - (8 << 30)
+        return self.fits_everywhere(need - self.opt.host_bytes)
+
+    def fits_everywhere(self, extra_host_bytes: int) -> bool:
+        """Can every local rank pin ``extra_host_bytes`` more (an equal share of
+        the host's available memory each, 8 GB kept free)?"""
+        local = int(os.environ.get("LOCAL_WORLD_SIZE", self.world))
+        ok = extra_host_bytes <= (host_available_bytes() - (8 << 30)) // max(1, local)
         return -self.max_over_ranks(-1.0 if ok else 0.0) >= 1.0
 
-    def tune(self, ratio: float, explore: int):
+    def tune(self, ratio: float, explore: int, opt=None, sizes=None):
         D = self.D
+        sizes = self.sizes if sizes is None else sizes
         slowdown = float(self.broadcast(self.profile_b200.LAST_RAW.get("link_slowdown_under_h1", 1.0)))
         rates = self.broadcast(self.profile_b200.host_rates())  # the fluid host-DRAM model ranks the strides
-        tuner = self.policy.StrideTuner(self.profile, self.sizes, range(1, 7), ratio, explore=explore,
+        tuner = self.policy.StrideTuner(self.profile, sizes, range(1, 7), ratio, explore=explore,
                                         link_slowdown=slowdown, placement=self.placement, rates=rates)
         tuner.queue = list(self.broadcast(tuner.queue))  # same exploration order on every rank
         while tuner.exploring:
             k = tuner.next_stride()
-            r = self.phase(tuner.plan_for(k))
+            r = self.phase(tuner.plan_for(k), opt=opt)
             tuner.record(k, self.max_over_ranks(r.measured.span_ns))
         return tuner
 
@@ -916,6 +930,120 @@ class B200Bench:
             "ms_per_step": ms, "value": self.P / (ms * 1e-3), "speedup_of_headline": ms / self.ms,
             "plan": "build_plan(N, ALL_CPU): CPU_UPDATE -> CPU_DOWNSCALE -> H2D_PARAMS16 chained"}
 
+    # BASELINE.json configs with more than one rank: (total params, ranks)
+    CONFIGS = {"13B/2": (13e9, 2), "20B/4": (20e9, 4), "20B/8": (20e9, 8), "70B/8": (70e9, 8)}
+    CONFIGS_FOR_N = {2: ["13B/2"], 4: ["20B/4"], 8: ["20B/8", "70B/8"]}
+
+    def release_headline_state(self) -> None:
+        """Free the headline shard (pinned pool, HBM residents, engines)
+        before the per-config runs allocate theirs."""
+        import gc
+
+        self.results = []
+        self.e2e_result = None
+        self.opt = None
+        gc.collect()
+        self.torch.cuda.synchronize()
+        self.torch.cuda.empty_cache()
+
+    def baseline_configs(self) -> None:
+        """BASELINE.json configs[2-4] on the ranks of this run: at N=2 the
+        13B/2 config, at N=4 20B/4, at N=8 20B/8 and the 70B/8 stride sweep
+        (``--configs`` picks others; a config needing more ranks than this run
+        has is run as rank slices, each process one rank of it).  Every
+        variant is timed under one stated HBM budget for both schedules: the
+        interleaved plan the tuner picks (explore-then-exploit) and the
+        reference's offload-to-CPU schedule (``build_plan(n, ALL_CPU)``,
+        scheduler.py:301-319) with the same residency — 0% (the paper's
+        offload premise, two HBM windows) and capacity-aware (as many
+        subgroups homed in HBM as fit).  ``target_20b_8``: north_star's >= 2x."""
+        names = [c for c in self.args.configs.split(",") if c] if self.args.configs is not None else \
+            self.CONFIGS_FOR_N.get(self.world, [])
+        self.out["baseline_configs"] = None
+        if not names:
+            return
+        self.release_headline_state()
+        out = {}
+        for name in names:
+            if name not in self.CONFIGS:
+                out[name] = {"skipped": f"unknown config (known: {sorted(self.CONFIGS)})"}
+                continue
+            total, ranks = self.CONFIGS[name]
+            total = int(total * self.args.config_scale)
+            if ranks % self.world and self.world != 1:
+                out[name] = {"skipped": f"{ranks} ranks do not split over a world of {self.world}"}
+                continue
+            out[name] = self.run_config(name, total, ranks, sweep=name == "70B/8")
+        self.out["baseline_configs"] = out
+        e = out.get("20B/8")
+        if isinstance(e, dict) and e.get("variants"):
+            v0 = next((v for v in e["variants"] if v.get("static_ratio") == 0.0 and "speedup_vs_all_cpu" in v), None)
+            best = max((v for v in e["variants"] if "speedup_vs_all_cpu" in v), key=lambda v: v["speedup_vs_all_cpu"],
+                       default=None)
+            self.out["target_20b_8"] = {
+                "target": 2.0, "ranks_run": e["ranks_run"], "of_ranks": e["ranks"],
+                "speedup_vs_all_cpu_at_0pct_resident": v0 and v0["speedup_vs_all_cpu"],
+                "met_at_0pct_resident": bool(v0 and v0["speedup_vs_all_cpu"] >= 2.0),
+                "best_speedup_vs_all_cpu": best and best["speedup_vs_all_cpu"],
+                "best_variant_static_ratio": best and best["static_ratio"]}
+
+    def run_config(self, name: str, total: int, ranks: int, sweep: bool) -> dict:
+        D, torch = self.D, self.torch
+        # this process's rank of the config (rank slices when the run has fewer ranks)
+        crank = self.rank if self.world == ranks else self.rank * (ranks // self.world)
+        mine = D.shard(total, ranks, self.SG)[crank]
+        sizes = [g.size for g in mine]
+        P_rank, nsg = sum(sizes), len(sizes)
+        entry = {"params": total, "ranks": ranks, "ranks_run": self.world, "rank_slices": self.world != ranks,
+                 "per_rank_params": P_rank, "subgroups_per_rank": nsg, "subgroup": self.SG, "variants": []}
+        steps = max(1, min(self.args.steps, self.args.config_steps))
+        free = torch.cuda.mem_get_info(self.device)[0]
+        auto = -self.max_over_ranks(-self.policy.capacity_static_ratio(sizes, free))
+        for ratio, label in ((0.0, "0% resident (two HBM windows)"), (auto, "capacity-aware")):
+            if label == "capacity-aware" and auto == 0.0:
+                continue
+            static = self.policy._quiet_plan(nsg, 1, ratio, self.placement).static_set
+            host_need = 16 * sum(s for i, s in enumerate(sizes) if i not in static)
+            v = {"static_ratio": ratio, "hbm_budget": label, "host_pinned_bytes_per_rank": host_need,
+                 "hbm_resident_state_bytes_per_rank": 12 * sum(sizes[i] for i in static)}
+            if not self.fits_everywhere(host_need):
+                v["skipped"] = "host-homed state would not fit in host memory on every local rank"
+                entry["variants"].append(v)
+                continue
+            opt = D.ShardedOptimizer.allocate(P_rank, self.SG, lowp=self.args.lowp, numa_node=self.numa,
+                                              host_homed=[i for i in range(nsg) if i not in static])
+            res = opt.to_device(self.device)
+            res.set_static(static)
+            fill_shard(opt, seed=4321 + crank, device=self.device)
+            tuner = self.tune(ratio, explore=3, opt=opt, sizes=sizes)
+            plan = tuner.plan()
+            self.phase(plan, opt=opt)
+            ms = self.timed(lambda: self.phase(plan, opt=opt), steps)
+            rplan = self.policy._quiet_plan(nsg, D.ALL_CPU, ratio, self.placement)
+            self.phase(rplan, opt=opt)
+            ref_ms = self.timed(lambda: self.phase(rplan, opt=opt), steps)
+            v.update({"stride": plan.stride, "ms_per_step": ms, "value": total / (ms * 1e-3),
+                      "all_cpu_ms_per_step": ref_ms, "all_cpu_value": total / (ref_ms * 1e-3),
+                      "speedup_vs_all_cpu": ref_ms / ms,
+                      "measured_ms_by_stride": {str(k): t / 1e6 for k, t in sorted(tuner.measured.items())}})
+            if sweep and ratio == 0.0:
+                # the GPU-subgroup-fraction sweep (configs[4]): every stride + ALL_CPU, one timed step each
+                sw = {}
+                for k in (1, 2, 3, 4, 5, 6):
+                    kp = self.policy._quiet_plan(nsg, k, ratio, self.placement)
+                    self.phase(kp, opt=opt)
+                    sw[str(k)] = self.timed(lambda: self.phase(kp, opt=opt), 1)
+                sw["all_cpu"] = ref_ms
+                v["stride_sweep_ms"] = sw
+            entry["variants"].append(v)
+            del opt, res, tuner
+            import gc
+
+            gc.collect()
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
+        return entry
+
     def traces(self) -> None:
         if self.rank != 0 or not self.args.trace_dir:
             return
@@ -980,6 +1108,7 @@ class B200Bench:
         self.copy_streams()
         self.reference_schedule()
         self.traces()
+        self.baseline_configs()
         if self.rank == 0:
             print(json.dumps(self.line()), flush=True)
         if self.world > 1:

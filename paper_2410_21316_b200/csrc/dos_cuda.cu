@@ -17,6 +17,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -401,10 +402,10 @@ __host__ __device__ constexpr uint32_t tma_stage_bytes() {
 
 // RS: the grads are the fused reduce-scatter of gs (16-bit grads only).  The
 // local rank's tile still arrives by TMA; every other rank's 4 elements of
-// this thread come over NVLink as one 8-byte load per rank, issued one tile
-// ahead (right after the current tile's are consumed) so their latency hides
-// behind this tile's update, stores and the next stage wait.
-template <int GT, int LT, int NT, int S, bool RS = false>
+// this thread come over NVLink as one 8-byte load per rank, issued RD tiles
+// ahead (right after a tile's are consumed, the loads of tile k + RD go out)
+// so their latency hides behind RD tiles' updates, stores and stage waits.
+template <int GT, int LT, int NT, int S, bool RS = false, int RD = 1>
 __global__ void __launch_bounds__(NT, 1)
     k_adam_tma(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
                const void* gv, uint16_t* __restrict__ w, int64_t ntiles, int64_t tail,
@@ -452,14 +453,24 @@ __global__ void __launch_bounds__(NT, 1)
   if (tid == 0)
     for (int64_t k = 0; k < S - 1 && k < mine; ++k) issue(k);
 
-  uint2 nx[RS ? DOS_MAX_PEERS + 1 : 1];  // the other ranks' grads of the next tile (RS)
-  auto rs_fetch = [&](int64_t k) {
+  // RS: the other ranks' grads of the next RD tiles, a register queue
+  // (nx[0] = the tile being updated; static indices only, so no local memory)
+  uint2 nx[RS ? RD : 1][RS ? DOS_MAX_PEERS + 1 : 1];
+  auto rs_fetch = [&](int64_t k, int slot) {
     const int64_t e0 = (first + k * step) * TE;
 #pragma unroll
-    for (int r = 0; r < (RS ? DOS_MAX_PEERS + 1 : 0); ++r)
-      if (r < gs.n && r != gs.self) nx[r] = __ldcs(reinterpret_cast<const uint2*>(gs.p[r] + e0) + tid);
+    for (int q = 0; q < (RS ? RD : 0); ++q)
+      if (q == slot) {
+#pragma unroll
+        for (int r = 0; r < (RS ? DOS_MAX_PEERS + 1 : 0); ++r)
+          if (r < gs.n && r != gs.self) nx[q][r] = __ldcs(reinterpret_cast<const uint2*>(gs.p[r] + e0) + tid);
+      }
   };
-  if (RS && mine > 0) rs_fetch(0);
+  if (RS) {
+#pragma unroll
+    for (int q = 0; q < RD; ++q)
+      if (q < mine) rs_fetch(q, q);
+  }
 
   for (int64_t k = 0; k < mine; ++k) {
     const int st = (int)(k % S);
@@ -489,17 +500,22 @@ __global__ void __launch_bounds__(NT, 1)
           if (r == gs.self) {
             x[0] = ge[0]; x[1] = ge[1]; x[2] = ge[2]; x[3] = ge[3];
           } else {
-            x[0] = widen16((uint16_t)(nx[r].x & 0xffffu), GT);
-            x[1] = widen16((uint16_t)(nx[r].x >> 16), GT);
-            x[2] = widen16((uint16_t)(nx[r].y & 0xffffu), GT);
-            x[3] = widen16((uint16_t)(nx[r].y >> 16), GT);
+            x[0] = widen16((uint16_t)(nx[0][r].x & 0xffffu), GT);
+            x[1] = widen16((uint16_t)(nx[0][r].x >> 16), GT);
+            x[2] = widen16((uint16_t)(nx[0][r].y & 0xffffu), GT);
+            x[3] = widen16((uint16_t)(nx[0][r].y >> 16), GT);
           }
 #pragma unroll
           for (int j = 0; j < 4; ++j) acc[j] = r ? __fadd_rn(acc[j], x[j]) : x[j];
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) ge[j] = rs_round(acc[j], GT, gs.scale);
-        if (k + 1 < mine) rs_fetch(k + 1);
+        // shift the queue and put tile k + RD's loads in flight
+#pragma unroll
+        for (int q = 0; q + 1 < RD; ++q)
+#pragma unroll
+          for (int r = 0; r < DOS_MAX_PEERS + 1; ++r) nx[q][r] = nx[q + 1][r];
+        if (k + RD < mine) rs_fetch(k + RD, RD - 1);
         // the reduced grads replace the local ones (as an NCCL reduce-scatter would leave them)
         const int64_t e0 = (first + k * step) * TE;
         __stcs(reinterpret_cast<uint2*>(const_cast<char*>(g) + e0 * GE) + tid,
@@ -559,7 +575,7 @@ __global__ void __launch_bounds__(NT, 1)
   if (tid == 0) bulk_wait_all();
 }
 
-template <int GT, int LT, int NT, int S, bool RS = false>
+template <int GT, int LT, int NT, int S, bool RS = false, int RD = 1>
 int launch_tma_cfg(float* p, float* m, float* v, const void* g, uint16_t* w, int64_t ntiles, int64_t tail,
                    const dos_kscal& s, int ctas_per_sm, cudaStream_t st, const dos_peers& pr,
                    const dos_gsrc& gs = dos_gsrc{0, 0, 1.0f, {}}) {
@@ -567,7 +583,7 @@ int launch_tma_cfg(float* p, float* m, float* v, const void* g, uint16_t* w, int
   static bool configured = false;
   if (!configured) {
     const cudaError_t e =
-        cudaFuncSetAttribute(k_adam_tma<GT, LT, NT, S, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_adam_tma<GT, LT, NT, S, RS, RD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return dos_set_error(DOS_ECUDA, "K1 smem attribute: %s", cudaGetErrorString(e));
     configured = true;
   }
@@ -579,7 +595,7 @@ int launch_tma_cfg(float* p, float* m, float* v, const void* g, uint16_t* w, int
     const char* e = getenv("DOS_K1_L2");
     return (e && strcmp(e, "evict_first") == 0) ? 1 : 0;
   }();
-  k_adam_tma<GT, LT, NT, S, RS><<<(unsigned)grid, NT, smem, st>>>(p, m, v, g, w, ntiles, tail, s, pr, l2ef, gs);
+  k_adam_tma<GT, LT, NT, S, RS, RD><<<(unsigned)grid, NT, smem, st>>>(p, m, v, g, w, ntiles, tail, s, pr, l2ef, gs);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return DOS_OK;
 }
@@ -641,6 +657,50 @@ int launch_adam_tma(float* p, float* m, float* v, const void* g, uint16_t* w, in
   return dos_set_error(DOS_EINVAL, "no K1 pipeline shape %d/%d", c.nt, c.stages);
 }
 
+// Fused reduce-scatter pipeline: shape (threads, stages, CTAs/SM) and how
+// many tiles ahead the peers' grads are loaded.  DOS_K1_RS=<shape>,<depth>:
+// shape 0 = 1024 x 3 x 1 (default), 1 = 512 x 6 x 1 (deeper TMA ring, more
+// registers per thread for the peer queue); depth 1 (default) or 2.
+// Swept with tools/k1_rs.py (profiles/r02_k1_rs_depth_shape.json).
+struct RsCfg {
+  int nt, stages, cpb, depth;
+};
+const RsCfg& rs_cfg() {
+  static RsCfg c = [] {
+    RsCfg r{1024, 3, 1, 1};
+    const char* e = getenv("DOS_K1_RS");
+    if (e) {
+      int shape = 0, depth = 1;
+      if (sscanf(e, "%d,%d", &shape, &depth) >= 1) {
+        if (shape == 1) r = RsCfg{512, 6, 1, 1};
+        r.depth = depth == 2 ? 2 : 1;
+      }
+    }
+    return r;
+  }();
+  return c;
+}
+
+template <int G, int L>
+int launch_rs_shape(float* p, float* m, float* v, const void* g, uint16_t* w, int64_t ntiles, int64_t tail,
+                    const dos_kscal& s, cudaStream_t st, const dos_peers& pr, const dos_gsrc& gs) {
+  const RsCfg& c = rs_cfg();
+  if (c.nt == 1024)
+    return c.depth == 2 ? launch_tma_cfg<G, L, 1024, 3, true, 2>(p, m, v, g, w, ntiles, tail, s, c.cpb, st, pr, gs)
+                        : launch_tma_cfg<G, L, 1024, 3, true, 1>(p, m, v, g, w, ntiles, tail, s, c.cpb, st, pr, gs);
+  return c.depth == 2 ? launch_tma_cfg<G, L, 512, 6, true, 2>(p, m, v, g, w, ntiles, tail, s, c.cpb, st, pr, gs)
+                      : launch_tma_cfg<G, L, 512, 6, true, 1>(p, m, v, g, w, ntiles, tail, s, c.cpb, st, pr, gs);
+}
+
+int launch_adam_tma_rs(int gt, int lt, float* p, float* m, float* v, const void* g, uint16_t* w, int64_t ntiles,
+                       int64_t tail, const dos_kscal& s, cudaStream_t st, const dos_peers& pr, const dos_gsrc& gs) {
+  if (gt == DOS_BF16 && lt == DOS_BF16) return launch_rs_shape<DOS_BF16, DOS_BF16>(p, m, v, g, w, ntiles, tail, s, st, pr, gs);
+  if (gt == DOS_F16 && lt == DOS_F16) return launch_rs_shape<DOS_F16, DOS_F16>(p, m, v, g, w, ntiles, tail, s, st, pr, gs);
+  if (gt == DOS_BF16 && lt == DOS_NONE) return launch_rs_shape<DOS_BF16, DOS_NONE>(p, m, v, g, w, ntiles, tail, s, st, pr, gs);
+  if (gt == DOS_F16 && lt == DOS_NONE) return launch_rs_shape<DOS_F16, DOS_NONE>(p, m, v, g, w, ntiles, tail, s, st, pr, gs);
+  return dos_set_error(DOS_ETYPE, "fused reduce-scatter: working copy must match the grad dtype (g=%d lowp=%d)", gt, lt);
+}
+
 }  // namespace
 
 dos_kscal dos_make_kscal(const dos_adam_scalars* s) {
@@ -699,7 +759,7 @@ int dos_adam_launch(float* p, float* m, float* v, const void* g, int gt, void* l
   // TMA path: a 16-byte-alignable range of at least one tile whose pipeline
   // shape fits in shared memory (all grad dtypes).  The fused reduce-scatter
   // always uses the default shape (1024 threads x 3 stages, one CTA per SM).
-  const int64_t tile = gs.n > 0 ? 4 * 1024 : 4 * tma_cfg().nt;
+  const int64_t tile = gs.n > 0 ? 4 * rs_cfg().nt : 4 * tma_cfg().nt;
   if ((gt == DOS_F32 || gt == DOS_F16 || gt == DOS_BF16) && (lt == DOS_NONE || lt == DOS_F16 || lt == DOS_BF16) &&
       head >= 0 && tma_enabled() && (gs.n > 0 || tma_fits(gt, lt)) && (n - head) / tile >= 1) {
     const int64_t ntiles = (n - head) / tile;
@@ -713,24 +773,8 @@ int dos_adam_launch(float* p, float* m, float* v, const void* g, int gt, void* l
     uint16_t* wb = lt == DOS_NONE ? nullptr : reinterpret_cast<uint16_t*>(lc + 2 * head);
     const dos_peers pb = dos_peers_offset(pr, head);
     if (gs.n > 0) {
-      // fused reduce-scatter: the default pipeline shape only (see k_adam_tma)
-      const dos_gsrc gsb = dos_gsrc_offset(gs, head);
-      const int cpb = 1;
-      if (gt == DOS_BF16 && lt == DOS_BF16)
-        rc = launch_tma_cfg<DOS_BF16, DOS_BF16, 1024, 3, true>(p + head, m + head, v + head, gb, wb, ntiles, tail, s,
-                                                              cpb, st, pb, gsb);
-      else if (gt == DOS_F16 && lt == DOS_F16)
-        rc = launch_tma_cfg<DOS_F16, DOS_F16, 1024, 3, true>(p + head, m + head, v + head, gb, wb, ntiles, tail, s,
-                                                            cpb, st, pb, gsb);
-      else if (gt == DOS_BF16 && lt == DOS_NONE)
-        rc = launch_tma_cfg<DOS_BF16, DOS_NONE, 1024, 3, true>(p + head, m + head, v + head, gb, wb, ntiles, tail, s,
-                                                              cpb, st, pb, gsb);
-      else if (gt == DOS_F16 && lt == DOS_NONE)
-        rc = launch_tma_cfg<DOS_F16, DOS_NONE, 1024, 3, true>(p + head, m + head, v + head, gb, wb, ntiles, tail, s,
-                                                             cpb, st, pb, gsb);
-      else
-        return dos_set_error(DOS_ETYPE, "fused reduce-scatter: working copy must match the grad dtype (g=%d lowp=%d)",
-                             gt, lt);
+      rc = launch_adam_tma_rs(gt, lt, p + head, m + head, v + head, gb, wb, ntiles, tail, s, st, pb,
+                              dos_gsrc_offset(gs, head));
       if (rc != DOS_OK) return rc;
       const cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return dos_set_error(DOS_ECUDA, "K1 (TMA, RS) launch failed: %s", cudaGetErrorString(e));
@@ -954,13 +998,33 @@ __global__ void __launch_bounds__(kThreads) k_coherence(const __grid_constant__ 
     const int64_t start = nw * win >= n ? k * win : (nw > 1 ? k * (n - win) / (nw - 1) : 0);
     const int64_t stop = start + win < n ? start + win : n;
     unsigned long long bad = 0, key = ~0ull;
-    for (int64_t i = start + threadIdx.x; i < stop; i += kThreads) {
-      if (to_lowp(b.p[r][i], b.lt) != b.w[r][i]) {
+    const float* P = b.p[r];
+    const uint16_t* W = b.w[r];
+    auto check = [&](float x, uint16_t y, int64_t i) {
+      if (to_lowp(x, b.lt) != y) {
         ++bad;
         const unsigned long long kk = ((unsigned long long)(b.base + r) << 40) | (unsigned long long)i;
         key = kk < key ? kk : key;
       }
+    };
+    int64_t i0 = start;
+    // 4 elements per load (16 B of p32, 8 B of working copy) where both align
+    if ((((uintptr_t)(P + start)) & 15u) == 0 && (((uintptr_t)(W + start)) & 7u) == 0) {
+      const int64_t nv = (stop - start) / 4;
+      const float4* P4 = reinterpret_cast<const float4*>(P + start);
+      const uint2* W4 = reinterpret_cast<const uint2*>(W + start);
+      for (int64_t j = threadIdx.x; j < nv; j += kThreads) {
+        const float4 pv = __ldcs(P4 + j);
+        const uint2 wv = __ldcs(W4 + j);
+        const int64_t e = start + 4 * j;
+        check(pv.x, (uint16_t)(wv.x & 0xffffu), e);
+        check(pv.y, (uint16_t)(wv.x >> 16), e + 1);
+        check(pv.z, (uint16_t)(wv.y & 0xffffu), e + 2);
+        check(pv.w, (uint16_t)(wv.y >> 16), e + 3);
+      }
+      i0 = start + 4 * nv;
     }
+    for (int64_t i = i0 + threadIdx.x; i < stop; i += kThreads) check(P[i], W[i], i);
     if (bad) {
       atomicAdd(out, bad);
       atomicMin(out + 1, key);

@@ -69,6 +69,7 @@ struct Engine {
   cudaStream_t st[3] = {nullptr, nullptr, nullptr};  // fast, h2d, d2h
   cudaStream_t gst = nullptr;                        // in-phase grad flush (D2H); host_io: residents' grads H2D
   cudaStream_t ost = nullptr;                        // host_io: residents' working copy D2H
+  cudaStream_t pst = nullptr;                        // fused all-gather: host subgroups' peer forwards
   std::vector<cudaEvent_t> ev_g;                      // per action: its grads are on the host
   std::vector<cudaEvent_t> ev_sg;                     // per subgroup: host_io grads of a static resident landed
   std::deque<int32_t> static_q;                       // host_io_ahead: resident updates whose grads are in flight
@@ -419,9 +420,16 @@ struct Engine {
       case DOS_H2D_PARAMS16:
         DOS_CU(cudaMemcpyAsync(dev_lowp + 2 * start, static_cast<const char*>(S.host_lowp) + 2 * start, (size_t)n * 2,
                                cudaMemcpyHostToDevice, s));
-        // fused all-gather for a host subgroup: forward it peer-to-peer (NVLink copy engine)
-        for (int r = 0; r < peers.n; ++r)
-          DOS_CU(cudaMemcpyAsync(peers.p[r] + start, dev_lowp + 2 * start, (size_t)n * 2, cudaMemcpyDeviceToDevice, s));
+        // fused all-gather for a host subgroup: forward it peer-to-peer (NVLink
+        // copy engines) on the peer stream, chained by event, so the next
+        // subgroup's prefetches on the H2D lane do not queue behind N-1 copies
+        if (peers.n > 0) {
+          DOS_CU(cudaEventRecord(ev_g[a->id], s));
+          DOS_CU(cudaStreamWaitEvent(pst, ev_g[a->id], 0));
+          for (int r = 0; r < peers.n; ++r)
+            DOS_CU(cudaMemcpyAsync(peers.p[r] + start, dev_lowp + 2 * start, (size_t)n * 2, cudaMemcpyDeviceToDevice,
+                                   pst));
+        }
         return DOS_OK;
       default:
         return dos_set_error(DOS_EINVAL, "unexpected action kind %d on a device lane", a->kind);
@@ -510,6 +518,7 @@ struct Engine {
     DOS_CU(cudaStreamWaitEvent(st[2], ev0, 0));
     DOS_CU(cudaStreamWaitEvent(gst, ev0, 0));
     DOS_CU(cudaStreamWaitEvent(ost, ev0, 0));
+    DOS_CU(cudaStreamWaitEvent(pst, ev0, 0));
     flush_q.clear();
     if (S.host_io) {
       // static residents' grads go H2D first thing, on the side stream, so
@@ -540,8 +549,8 @@ struct Engine {
     }
     active = false;
     cudaError_t ce = cudaSuccess;
-    for (int i = 0; i < 5; ++i) {
-      cudaError_t e = cudaStreamSynchronize(i < 3 ? st[i] : i == 3 ? gst : ost);
+    for (int i = 0; i < 6; ++i) {
+      cudaError_t e = cudaStreamSynchronize(i < 3 ? st[i] : i == 3 ? gst : i == 4 ? ost : pst);
       if (e != cudaSuccess && ce == cudaSuccess) ce = e;
     }
     if (ce != cudaSuccess) return dos_set_error(DOS_ECUDA, "update phase failed on the device: %s", cudaGetErrorString(ce));
@@ -578,6 +587,7 @@ struct Engine {
     for (int i = 0; i < 3; ++i) DOS_CU(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking));
     DOS_CU(cudaStreamCreateWithFlags(&gst, cudaStreamNonBlocking));
     DOS_CU(cudaStreamCreateWithFlags(&ost, cudaStreamNonBlocking));
+    DOS_CU(cudaStreamCreateWithFlags(&pst, cudaStreamNonBlocking));
     DOS_CU(cudaEventCreate(&ev0));
     if (slot_elems > 0) DOS_CU(cudaMalloc(reinterpret_cast<void**>(&slot_mem), (size_t)nslots * 3 * slot_elems * 4));
     cudaDriverEntryPointQueryResult qr;
@@ -604,7 +614,7 @@ struct Engine {
         cudaStreamSynchronize(st[i]);
         cudaStreamDestroy(st[i]);
       }
-    for (cudaStream_t side : {gst, ost})
+    for (cudaStream_t side : {gst, ost, pst})
       if (side) {
         cudaStreamSynchronize(side);
         cudaStreamDestroy(side);

@@ -256,6 +256,7 @@ def execute_plan(
 # from the first element to the last (ragged tails included), per subgroup
 COHERENCE_WINDOW = 2048
 COHERENCE_WINDOWS = 16
+COHERENCE_FULL_WINDOW = 1 << 16  # whole-subgroup checks: one CTA per 64K elements
 
 
 def _coherence_mode(check) -> str:
@@ -291,7 +292,7 @@ def check_coherence_after_phase(opt: ShardedOptimizer, res, mode: str = "sampled
     ranges, names = [], []
 
     def add(p_ptr: int, w_ptr: int, n: int, whole: bool, what: str):
-        win = COHERENCE_WINDOW
+        win = COHERENCE_FULL_WINDOW if whole else COHERENCE_WINDOW
         nwin = -(-n // win) if whole else COHERENCE_WINDOWS
         ranges.append(N.dos_coh_range(p_ptr, w_ptr, n, win, nwin))
         names.append(what)

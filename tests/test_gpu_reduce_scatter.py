@@ -149,3 +149,20 @@ def test_fused_reduce_scatter_requires_in_phase_flush(h100):
     bad = GradSources((res.grads.data_ptr() + 2,), 0, 1.0)  # src_g[self] must be dev_g
     with pytest.raises(ValueError):
         D.execute_plan(opt, plan, h100, HYPER, flush_grads=True, grad_sources=bad)
+
+
+@pytest.mark.parametrize("cfg", ["0,2", "1,1", "1,2"])
+def test_rs_pipeline_shapes_and_depths_bit_exact(cfg):
+    """Every selectable fused-RS pipeline (DOS_K1_RS=<shape>,<depth>: 512x6
+    ring, peer loads 2 tiles ahead) gives the same bits as the default."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, DOS_K1_RS=cfg)
+    proc = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                           str(Path(__file__)), "-k", "test_k1_fused_reduce_scatter and not fp16-1-0"],
+                          cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert proc.returncode == 0 and " passed" in proc.stdout, proc.stdout[-3000:]

@@ -1,10 +1,12 @@
-"""K1 with the reduce-scatter fused in (dos_adam_step_cuda_rs) vs plain K1,
+"""K1 with the reduce-scatter fused in (pipeline shape / peer-prefetch depth
+from DOS_K1_RS, see tools/k1_rs_sweep.sh) (dos_adam_step_cuda_rs) vs plain K1,
 and the stand-alone reduce kernel, on one B200.  The "ranks" are separate
 local HBM buffers, so this measures the kernel's HBM efficiency with the
 extra grad streams (on a real node the peers' reads go over NVLink instead).
 Algorithmic bytes per param: K1 28; K1+RS 28 + 2*(world-1) (other ranks'
 grads) + 2 (reduced grads written back); reduce 2*world + 2."""
 import json
+import os
 import sys
 
 sys.path.insert(0, ".")
@@ -38,7 +40,7 @@ def timed(run, reps=10):
     return float(np.median(ts))
 
 
-out = {}
+out = {"DOS_K1_RS": os.environ.get("DOS_K1_RS", "0,1 (default: 1024 x 3 ring, peers 1 tile ahead)")}
 st = lambda: torch.cuda.current_stream().cuda_stream
 t = timed(lambda: N.check(lib.dos_adam_step_cuda(p.data_ptr(), m.data_ptr(), v.data_ptr(), gs[0].data_ptr(),
                                                  N.DOS_BF16, w.data_ptr(), N.DOS_BF16, n, sc, st())))
