@@ -980,12 +980,18 @@ class B200Bench:
             v0 = next((v for v in e["variants"] if v.get("static_ratio") == 0.0 and "speedup_vs_all_cpu" in v), None)
             best = max((v for v in e["variants"] if "speedup_vs_all_cpu" in v), key=lambda v: v["speedup_vs_all_cpu"],
                        default=None)
+            cap = next((v for v in e["variants"] if "speedup_vs_offload_to_cpu_at_0pct" in v), None)
             self.out["target_20b_8"] = {
                 "target": 2.0, "ranks_run": e["ranks_run"], "of_ranks": e["ranks"],
+                "rank_slices": e["rank_slices"],
+                # north_star's criterion on the offload premise: both schedules with no HBM residents
                 "speedup_vs_all_cpu_at_0pct_resident": v0 and v0["speedup_vs_all_cpu"],
                 "met_at_0pct_resident": bool(v0 and v0["speedup_vs_all_cpu"] >= 2.0),
-                "best_speedup_vs_all_cpu": best and best["speedup_vs_all_cpu"],
-                "best_variant_static_ratio": best and best["static_ratio"]}
+                "best_speedup_vs_all_cpu_same_residency": best and best["speedup_vs_all_cpu"],
+                "best_variant_static_ratio": best and best["static_ratio"],
+                # capacity-aware residency against the pure offload-to-CPU schedule
+                "capacity_aware_vs_offload_to_cpu": cap and cap["speedup_vs_offload_to_cpu_at_0pct"],
+                "capacity_aware_static_ratio": cap and cap["static_ratio"]}
 
     def run_config(self, name: str, total: int, ranks: int, sweep: bool) -> dict:
         D, torch = self.D, self.torch
@@ -999,6 +1005,7 @@ class B200Bench:
         steps = max(1, min(self.args.steps, self.args.config_steps))
         free = torch.cuda.mem_get_info(self.device)[0]
         auto = -self.max_over_ranks(-self.policy.capacity_static_ratio(sizes, free))
+        offload_ms = None
         for ratio, label in ((0.0, "0% resident (two HBM windows)"), (auto, "capacity-aware")):
             if label == "capacity-aware" and auto == 0.0:
                 continue
@@ -1024,8 +1031,15 @@ class B200Bench:
             ref_ms = self.timed(lambda: self.phase(rplan, opt=opt), steps)
             v.update({"stride": plan.stride, "ms_per_step": ms, "value": total / (ms * 1e-3),
                       "all_cpu_ms_per_step": ref_ms, "all_cpu_value": total / (ref_ms * 1e-3),
+                      # same HBM budget for both schedules (the residents update on the GPU in both)
                       "speedup_vs_all_cpu": ref_ms / ms,
                       "measured_ms_by_stride": {str(k): t / 1e6 for k, t in sorted(tuner.measured.items())}})
+            if ratio == 0.0:
+                offload_ms = ref_ms  # the reference's pure offload-to-CPU schedule (ZeRO-3 offload)
+            elif offload_ms is not None:
+                # this residency against the pure offload-to-CPU schedule (which keeps
+                # no state in HBM): what capacity-aware residency buys, stated as such
+                v["speedup_vs_offload_to_cpu_at_0pct"] = offload_ms / ms
             if sweep and ratio == 0.0:
                 # the GPU-subgroup-fraction sweep (configs[4]): every stride + ALL_CPU, one timed step each
                 sw = {}

@@ -28,8 +28,10 @@
 // update and flush (the plan itself is unchanged).
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
@@ -44,6 +46,27 @@
 namespace {
 
 typedef CUresult (*pfn_wait_value32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*pfn_write_value32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+// Working-copy staging ring of the host lane (dos_host_adam_ring): slots x
+// chunk elements of pinned memory, small enough to stay in the host's LLC.
+// DOS_W_RING=0 turns it off (H1 then writes the working copy into the host
+// image with non-temporal stores and H2D_PARAMS16 ships it from there).
+struct RingCfg {
+  bool on;
+  int slots;
+  int64_t chunk;
+};
+const RingCfg& ring_cfg() {
+  static RingCfg c = [] {
+    RingCfg r{true, 4, 1 << 19};  // 4 x 512K elements (4 MB of bf16)
+    if (const char* e = getenv("DOS_W_RING")) r.on = strcmp(e, "0") != 0;
+    if (const char* e = getenv("DOS_W_RING_SLOTS")) r.slots = std::max(2, std::min(64, atoi(e)));
+    if (const char* e = getenv("DOS_W_RING_CHUNK")) r.chunk = std::max<int64_t>(4096, atoll(e)) & ~int64_t(63);
+    return r;
+  }();
+  return c;
+}
 
 int64_t now_ns() {
   return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
@@ -70,6 +93,18 @@ struct Engine {
   cudaStream_t gst = nullptr;                        // in-phase grad flush (D2H); host_io: residents' grads H2D
   cudaStream_t ost = nullptr;                        // host_io: residents' working copy D2H
   cudaStream_t pst = nullptr;                        // fused all-gather: host subgroups' peer forwards
+  cudaStream_t wst = nullptr;                        // staging ring: working-copy chunks H2D
+  // staging ring (see RingCfg); ring_phase: used in this phase
+  bool ring_phase = false;
+  uint16_t* ring_mem = nullptr;
+  std::vector<cudaEvent_t> ring_ev;                   // per slot: its last shipped chunk has left the host
+  std::vector<uint8_t> ring_ev_live;
+  int64_t ring_next = 0;                              // chunks shipped so far (the ring runs on across subgroups)
+  int64_t ring_sg_start = 0;                          // subgroup being shipped
+  uint32_t* ring_flags = nullptr;                     // mapped: per subgroup, epoch once its last chunk landed
+  CUdeviceptr ring_flags_dev = 0;
+  int32_t ring_flags_cap = 0;
+  pfn_write_value32 write_fn = nullptr;
   std::vector<cudaEvent_t> ev_g;                      // per action: its grads are on the host
   std::vector<cudaEvent_t> ev_sg;                     // per subgroup: host_io grads of a static resident landed
   std::deque<int32_t> static_q;                       // host_io_ahead: resident updates whose grads are in flight
@@ -182,8 +217,40 @@ struct Engine {
     }
   }
 
+  // staging-ring callbacks (run on the host worker = team thread 0)
+  static int ring_ship(void* ctx, int64_t, int slot, int64_t off, int64_t cnt) {
+    Engine* e = static_cast<Engine*>(ctx);
+    const RingCfg& rc = ring_cfg();
+    char* dst = static_cast<char*>(e->S.dev_lowp) + 2 * (e->ring_sg_start + off);
+    DOS_CU(cudaMemcpyAsync(dst, e->ring_mem + (int64_t)slot * rc.chunk, (size_t)cnt * 2, cudaMemcpyHostToDevice, e->wst));
+    DOS_CU(cudaEventRecord(e->ring_ev[slot], e->wst));
+    e->ring_ev_live[slot] = 1;
+    return DOS_OK;
+  }
+  static int ring_reclaim(void* ctx, int slot) {
+    Engine* e = static_cast<Engine*>(ctx);
+    if (e->ring_ev_live[slot]) DOS_CU(cudaEventSynchronize(e->ring_ev[slot]));
+    e->ring_ev_live[slot] = 0;
+    return DOS_OK;
+  }
+
   int run_host(const Job& j, std::string& msg) {
     const int lt = S.lowp_dtype;
+    if (j.kind == DOS_CPU_UPDATE && ring_phase) {
+      // the working copy leaves through the LLC-resident staging ring; its
+      // last chunk's landing is published per subgroup for H2D_PARAMS16
+      const int64_t a = sg_start[j.sg], n = sg_size[j.sg];
+      const RingCfg& rc = ring_cfg();
+      dos_ring r{ring_mem, rc.slots, rc.chunk, ring_next, this, ring_ship, ring_reclaim};
+      ring_sg_start = a;
+      int code = dos_host_adam_ring(S.host_p + a, S.host_m + a, S.host_v + a, static_cast<const char*>(S.host_g) + 2 * a,
+                                    lt, lt, n, K, host_threads, r);
+      ring_next += (n + rc.chunk - 1) / rc.chunk;
+      if (code == DOS_OK && write_fn(( CUstream)wst, ring_flags_dev + 4 * (CUdeviceptr)j.sg, epoch, 0) != CUDA_SUCCESS)
+        code = dos_set_error(DOS_ECUDA, "cuStreamWriteValue32 (staging ring) failed");
+      if (code != DOS_OK) msg = dos_last_error();
+      return code;
+    }
     if (j.kind == DOS_CPU_UPDATE) {
       const int64_t a = sg_start[j.sg], n = sg_size[j.sg];
       const void* g = static_cast<const char*>(S.host_g) + 2 * a;
@@ -418,8 +485,15 @@ struct Engine {
         return DOS_OK;
       }
       case DOS_H2D_PARAMS16:
-        DOS_CU(cudaMemcpyAsync(dev_lowp + 2 * start, static_cast<const char*>(S.host_lowp) + 2 * start, (size_t)n * 2,
-                               cudaMemcpyHostToDevice, s));
+        if (ring_phase) {
+          // the chunks already went H2D through the staging ring during the
+          // CPU update: wait until its last one has landed
+          if (wait_fn((CUstream)s, ring_flags_dev + 4 * (CUdeviceptr)sg, epoch, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+            return dos_set_error(DOS_ECUDA, "cuStreamWaitValue32 (staging ring) failed");
+        } else {
+          DOS_CU(cudaMemcpyAsync(dev_lowp + 2 * start, static_cast<const char*>(S.host_lowp) + 2 * start, (size_t)n * 2,
+                                 cudaMemcpyHostToDevice, s));
+        }
         // fused all-gather for a host subgroup: forward it peer-to-peer (NVLink
         // copy engines) on the peer stream, chained by event, so the next
         // subgroup's prefetches on the H2D lane do not queue behind N-1 copies
@@ -493,10 +567,36 @@ struct Engine {
       flags_cap = want;
       epoch = 0;
     }
+    if (ring_flags_cap < ns) {
+      if (ring_flags) cudaFreeHost(ring_flags);
+      ring_flags = nullptr;
+      const int32_t want = std::max(ns, 256);
+      DOS_CU(cudaHostAlloc(reinterpret_cast<void**>(&ring_flags), (size_t)want * 4, cudaHostAllocMapped));
+      memset(ring_flags, 0, (size_t)want * 4);
+      void* dptr = nullptr;
+      DOS_CU(cudaHostGetDevicePointer(&dptr, ring_flags, 0));
+      ring_flags_dev = (CUdeviceptr)dptr;
+      ring_flags_cap = want;
+      // flags written in earlier epochs must not satisfy this phase's waits
+      memset(flags, 0, (size_t)flags_cap * 4);
+      epoch = 0;
+    }
     ++epoch;
     if (epoch == 0) {  // wrapped: reset
       memset(flags, 0, (size_t)flags_cap * 4);
+      memset(ring_flags, 0, (size_t)ring_flags_cap * 4);
       epoch = 1;
+    }
+    // the staging ring carries the working copy of host-updated subgroups in
+    // the device-resident mode with the downscale fused (host_io mirrors the
+    // working copy into the host image instead)
+    ring_phase = ring_cfg().on && fuse && !S.host_io && wait_fn && write_fn && wait_value_ok;
+    if (ring_phase && !ring_mem) {
+      const RingCfg& rc = ring_cfg();
+      DOS_CU(cudaHostAlloc(reinterpret_cast<void**>(&ring_mem), (size_t)rc.slots * rc.chunk * 2, cudaHostAllocDefault));
+      ring_ev.resize(rc.slots);
+      ring_ev_live.assign(rc.slots, 0);
+      for (auto& e : ring_ev) DOS_CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     max_actions = cap;
     count = 0;
@@ -519,6 +619,7 @@ struct Engine {
     DOS_CU(cudaStreamWaitEvent(gst, ev0, 0));
     DOS_CU(cudaStreamWaitEvent(ost, ev0, 0));
     DOS_CU(cudaStreamWaitEvent(pst, ev0, 0));
+    DOS_CU(cudaStreamWaitEvent(wst, ev0, 0));
     flush_q.clear();
     if (S.host_io) {
       // static residents' grads go H2D first thing, on the side stream, so
@@ -549,8 +650,8 @@ struct Engine {
     }
     active = false;
     cudaError_t ce = cudaSuccess;
-    for (int i = 0; i < 6; ++i) {
-      cudaError_t e = cudaStreamSynchronize(i < 3 ? st[i] : i == 3 ? gst : i == 4 ? ost : pst);
+    for (int i = 0; i < 7; ++i) {
+      cudaError_t e = cudaStreamSynchronize(i < 3 ? st[i] : i == 3 ? gst : i == 4 ? ost : i == 5 ? pst : wst);
       if (e != cudaSuccess && ce == cudaSuccess) ce = e;
     }
     if (ce != cudaSuccess) return dos_set_error(DOS_ECUDA, "update phase failed on the device: %s", cudaGetErrorString(ce));
@@ -588,6 +689,7 @@ struct Engine {
     DOS_CU(cudaStreamCreateWithFlags(&gst, cudaStreamNonBlocking));
     DOS_CU(cudaStreamCreateWithFlags(&ost, cudaStreamNonBlocking));
     DOS_CU(cudaStreamCreateWithFlags(&pst, cudaStreamNonBlocking));
+    DOS_CU(cudaStreamCreateWithFlags(&wst, cudaStreamNonBlocking));
     DOS_CU(cudaEventCreate(&ev0));
     if (slot_elems > 0) DOS_CU(cudaMalloc(reinterpret_cast<void**>(&slot_mem), (size_t)nslots * 3 * slot_elems * 4));
     cudaDriverEntryPointQueryResult qr;
@@ -595,6 +697,12 @@ struct Engine {
     if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &qr) == cudaSuccess &&
         qr == cudaDriverEntryPointSuccess)
       wait_fn = reinterpret_cast<pfn_wait_value32>(fn);
+    else
+      cudaGetLastError();
+    fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      write_fn = reinterpret_cast<pfn_write_value32>(fn);
     else
       cudaGetLastError();
     worker = std::thread([this] { worker_loop(); });
@@ -614,7 +722,7 @@ struct Engine {
         cudaStreamSynchronize(st[i]);
         cudaStreamDestroy(st[i]);
       }
-    for (cudaStream_t side : {gst, ost, pst})
+    for (cudaStream_t side : {gst, ost, pst, wst})
       if (side) {
         cudaStreamSynchronize(side);
         cudaStreamDestroy(side);
@@ -626,6 +734,9 @@ struct Engine {
     if (ev0) cudaEventDestroy(ev0);
     if (slot_mem) cudaFree(slot_mem);
     if (flags) cudaFreeHost(flags);
+    if (ring_flags) cudaFreeHost(ring_flags);
+    for (auto e : ring_ev) cudaEventDestroy(e);
+    if (ring_mem) cudaFreeHost(ring_mem);
   }
 };
 

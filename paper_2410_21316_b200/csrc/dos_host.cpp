@@ -206,6 +206,73 @@ int dos_host_adam(float* p, float* m, float* v, const void* g, int gt, void* lp,
   return DOS_OK;
 }
 
+namespace {
+// Sense-reversing spin barrier for the k threads of one team job (the
+// per-chunk sync of the staging ring: ~1 us, where the team's own fork-join
+// would cost a condition-variable round trip per chunk).
+class SpinBarrier {
+ public:
+  explicit SpinBarrier(int k) : k_(k) {}
+  void arrive_and_wait() {
+    const int g = gen_.load(std::memory_order_acquire);
+    if (count_.fetch_add(1, std::memory_order_acq_rel) == k_ - 1) {
+      count_.store(0, std::memory_order_relaxed);
+      gen_.store(g + 1, std::memory_order_release);
+      return;
+    }
+    while (gen_.load(std::memory_order_acquire) == g) __builtin_ia32_pause();
+  }
+
+ private:
+  const int k_;
+  std::atomic<int> count_{0};
+  std::atomic<int> gen_{0};
+};
+}  // namespace
+
+int dos_host_adam_ring(float* p, float* m, float* v, const void* g, int gt, int lt, int64_t n, const dos_kscal& s,
+                       int nthreads, const dos_ring& ring) {
+  if (n == 0) return DOS_OK;
+  if (lt == DOS_NONE || ring.nslots < 2 || ring.chunk < 64 || !ring.slots || !ring.ship || !ring.reclaim)
+    return dos_set_error(DOS_EINVAL, "staging ring: bad configuration");
+  const dos_hk_table& t = hk();
+  const std::shared_ptr<Team> hold = team();
+  Team& tm = *hold;
+  int k = nthreads > 0 ? std::min(nthreads, tm.size()) : tm.size();
+  const int64_t nchunks = (n + ring.chunk - 1) / ring.chunk;
+  const int gsz = gt == DOS_F32 ? 4 : 2;
+  auto slot_of = [&](int64_t c) { return (int)((ring.first + c) % ring.nslots); };
+  // the slot of chunk 0 may still be shipping the previous subgroup's last chunks
+  const int rc0 = ring.reclaim(ring.ctx, slot_of(0));
+  if (rc0 != DOS_OK) return rc0;
+  SpinBarrier bar(k);
+  std::atomic<int> err{DOS_OK};
+  tm.run(k, [&](int tid) {
+    for (int64_t c = 0; c < nchunks; ++c) {
+      const int64_t c0 = c * ring.chunk, len = std::min(ring.chunk, n - c0);
+      const int slot = slot_of(c);
+      // this thread's slice of the chunk, 64-element aligned
+      const int64_t per = ((len + k - 1) / k + 63) & ~int64_t(63);
+      const int64_t lo = std::min<int64_t>(len, per * tid), hi = std::min<int64_t>(len, lo + per);
+      if (lo < hi)
+        t.adam_cached(p + c0, m + c0, v + c0, static_cast<const char*>(g) + gsz * c0, gt,
+                      ring.slots + (int64_t)slot * ring.chunk, lt, lo, hi, s);
+      if (tid == 0 && c + 1 < nchunks && err.load(std::memory_order_relaxed) == DOS_OK) {
+        // the slot chunk c + 1 writes must have left the host (its copy,
+        // shipped nslots - 1 chunks ago) before anyone starts chunk c + 1
+        const int rc = ring.reclaim(ring.ctx, slot_of(c + 1));
+        if (rc != DOS_OK) err.store(rc);
+      }
+      bar.arrive_and_wait();
+      if (tid == 0 && err.load(std::memory_order_relaxed) == DOS_OK) {
+        const int rc = ring.ship(ring.ctx, c, slot, c0, len);
+        if (rc != DOS_OK) err.store(rc);
+      }
+    }
+  });
+  return err.load();
+}
+
 int dos_host_down(const float* x, void* out, int ot, int64_t n, int nthreads) {
   const dos_hk_table& t = hk();
   parallel_chunks(n, nthreads, [&](int64_t lo, int64_t hi) { t.down(x, out, ot, lo, hi); });

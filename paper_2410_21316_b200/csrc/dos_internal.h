@@ -56,7 +56,30 @@ struct dos_hk_table {
   void (*adam)(float*, float*, float*, const void*, int, void*, int, int64_t, int64_t, const dos_kscal&);
   void (*down)(const float*, void*, int, int64_t, int64_t);
   void (*up)(const void*, int, float*, int64_t, int64_t);
+  void (*adam_cached)(float*, float*, float*, const void*, int, void*, int, int64_t, int64_t, const dos_kscal&);
 };
+
+// H1 through a staging ring (the working copy of host-updated subgroups):
+// the subgroup is processed in chunks of `chunk` elements by the whole team;
+// chunk c's working copy goes (regular stores) into ring slot
+// (first + c) % nslots, and after the team's barrier thread 0 calls
+// ship(ctx, c, slot, offset, count) — the engine enqueues the slot's H2D copy —
+// while the other threads
+// already work on chunk c + 1.  Before chunk c + 1's barrier, thread 0 calls
+// reclaim(ctx, slot) for the slot chunk c + 1 writes (waits until its
+// previous copy has left the host).  Small slots stay in the LLC, so the
+// working copy never makes a host-DRAM round trip.
+struct dos_ring {
+  uint16_t* slots;  // nslots * chunk elements, pinned
+  int nslots;
+  int64_t chunk;
+  int64_t first;    // chunk 0 goes to slot first % nslots (the ring runs on across subgroups)
+  void* ctx;
+  int (*ship)(void* ctx, int64_t chunk_index, int slot, int64_t offset, int64_t count);
+  int (*reclaim)(void* ctx, int slot);
+};
+int dos_host_adam_ring(float* p, float* m, float* v, const void* g, int gt, int lt, int64_t n, const dos_kscal& s,
+                       int nthreads, const dos_ring& ring);
 extern const dos_hk_table dos_hk_avx512;
 extern const dos_hk_table dos_hk_avx2;
 extern const dos_hk_table dos_hk_generic;
