@@ -2,9 +2,10 @@
 
 Restates the update-phase part of pkg/src/optistate/sim.py (SimTarget
 :64-133, Timeline/_build_timeline :136-171, simulate_update_phase :174-183,
-memory_trace :186-223, the grad-flush rate model :226-268 and sweep_stride
-:505-550) with identical integer-ns arithmetic, so predicted timelines match
-the reference's frozen makespans exactly.
+memory_trace :186-223 and the grad-flush rate model :226-268) with identical
+integer-ns arithmetic, so predicted timelines match the reference's frozen
+makespans exactly.  The reference's offline analysis drivers (sweep_stride,
+simulate_iteration, compare_approaches, sim.py:271-550) are out of scope.
 
 Makespan is the last end over the compute lanes; transfers after it (the
 final half-precision H2D) are ``spillover``.  The B200 report states both
@@ -15,13 +16,12 @@ from __future__ import annotations
 
 import enum
 import math
-from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 from typing import Iterable, Sequence
 
 from .engine import run_update, validate_schedule
-from .perfmodel import ALL_CPU, plan_stride_for
-from .plan import COMPUTE_LANES, Action, ActionKind, Lane, ScheduledAction, UpdatePlan, build_plan
+from .perfmodel import ALL_CPU
+from .plan import COMPUTE_LANES, Action, ActionKind, Lane, ScheduledAction, UpdatePlan
 from .state import (
     GRADS16_BYTES_PER_PARAM,
     MODEL16_BYTES_PER_PARAM,
@@ -200,52 +200,8 @@ def grad_flush_throughput(strategy: GradFlushStrategy, profile: SystemProfile,
     raise ValueError(f"unknown strategy {strategy!r}")
 
 
-@dataclass(frozen=True)
-class SweepEntry:
-    k: int
-    stride: int
-    makespan_ns: int
-    spillover_ns: int
-    per_subgroup_ns: float
-
-
-@dataclass(frozen=True)
-class SweepResult:
-    profile_name: str
-    num_subgroups: int
-    subgroup_size: int
-    entries: tuple[SweepEntry, ...]
-
-    @property
-    def best_k(self) -> int:
-        return min(self.entries, key=lambda e: e.makespan_ns).k
-
-
-def sweep_stride(profile: SystemProfile, num_subgroups: int, subgroup_size: int,
-                 k_values: Iterable[int] = range(1, 7), jobs: int = 1) -> SweepResult:
-    """Predicted makespan per analysis ratio k (plan stride k + 1)."""
-    ks = list(k_values)
-    for k in ks:
-        if not isinstance(k, int) or k < 1:
-            raise ValueError(f"sweep ratios must be ints >= 1, got {k!r}")
-    if jobs < 1:
-        raise ValueError("jobs must be >= 1")
-
-    def one(k: int) -> SweepEntry:
-        tl = simulate_update_phase(build_plan(num_subgroups, plan_stride_for(k)), profile, subgroup_size)
-        return SweepEntry(k=k, stride=k + 1, makespan_ns=tl.makespan_ns, spillover_ns=tl.spillover_ns,
-                          per_subgroup_ns=tl.makespan_ns / num_subgroups if num_subgroups else 0.0)
-
-    if jobs == 1 or len(ks) <= 1:
-        entries = [one(k) for k in ks]
-    else:
-        with ThreadPoolExecutor(max_workers=jobs) as pool:
-            entries = list(pool.map(one, ks))
-    return SweepResult(profile.name, num_subgroups, subgroup_size, tuple(entries))
-
-
 __all__ = [
-    "ALL_CPU", "GradFlushStrategy", "SimTarget", "SweepEntry", "SweepResult", "Timeline", "build_timeline",
-    "grad_flush_throughput", "memory_trace", "normalize_sizes", "simulate_update_phase", "sweep_stride",
+    "ALL_CPU", "GradFlushStrategy", "SimTarget", "Timeline", "build_timeline",
+    "grad_flush_throughput", "memory_trace", "normalize_sizes", "simulate_update_phase",
     "GRADS16_BYTES_PER_PARAM",
 ]

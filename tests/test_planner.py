@@ -295,13 +295,6 @@ def test_grad_flush_rates(h100):
     assert fast == pytest.approx(26_883_910_386.97, rel=1e-6)
 
 
-def test_sweep_orders_v100(v100):
-    res = D.sweep_stride(v100, 60, 10**8, k_values=[2, 3, 4, 5], jobs=2)
-    spans = [e.makespan_ns for e in res.entries]
-    assert spans == sorted(spans) and len(set(spans)) == 4
-    assert res.best_k == 2
-
-
 # ------------------------------------------------------------------ B200 policy
 
 
