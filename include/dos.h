@@ -244,6 +244,10 @@ typedef struct dos_state_desc {
    * ahead of the fast lane, so the copy engine interleaves them with the
    * H2D lane instead of draining them all first (best when they lead). */
   int32_t host_io_ahead;
+  /* How many CPU_UPDATE actions the plan holds (-1: unknown).  0 lets the
+   * engine skip the host lane's staging-ring shuttle for this phase (plans
+   * with no host-updated subgroup keep every SM for K1). */
+  int32_t host_updates;
 } dos_state_desc;
 
 #define DOS_MAX_PEERS 7

@@ -64,6 +64,7 @@ class dos_state_desc(C.Structure):
         ("grad_scale", C.c_float),
         ("dev_static_sg", C.POINTER(C.c_void_p)),
         ("host_io_ahead", C.c_int32),
+        ("host_updates", C.c_int32),
     ]
 
 

@@ -21,6 +21,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <atomic>
 
 #include "dos_internal.h"
@@ -29,6 +30,7 @@
 namespace {
 
 std::atomic<int64_t> g_launches{0};  // every libdos kernel launch (dos_launch_count)
+std::atomic<int> g_reserved_sms{0};  // SMs a running shuttle occupies (K1's persistent grid leaves them out)
 
 constexpr int kThreads = 256;
 constexpr int kVec = 8;  // elements per thread per trip
@@ -587,7 +589,7 @@ int launch_tma_cfg(float* p, float* m, float* v, const void* g, uint16_t* w, int
     if (e != cudaSuccess) return dos_set_error(DOS_ECUDA, "K1 smem attribute: %s", cudaGetErrorString(e));
     configured = true;
   }
-  const int64_t cap = (int64_t)sm_count() * ctas_per_sm;
+  const int64_t cap = (int64_t)std::max(1, sm_count() - g_reserved_sms.load(std::memory_order_relaxed)) * ctas_per_sm;
   const int64_t grid = ntiles < cap ? ntiles : cap;
   // DOS_K1_L2=evict_first turns on L2 evict-first hints for the bulk copies;
   // measured on the B200 they do not help (alone or under duplex DMA), so off.
@@ -1081,5 +1083,123 @@ extern "C" int dos_coherence_cuda(const dos_coh_range* ranges, int nranges, int 
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return dos_set_error(DOS_ECUDA, "coherence launch failed: %s", cudaGetErrorString(e));
   }
+  return DOS_OK;
+}
+
+// ---------------------------------------------------------------- shuttle
+// The host lane's copy engine for small, LLC-resident staging slots: a
+// persistent kernel of a few CTAs, launched at phase start, that serves a
+// descriptor queue in mapped pinned host memory (dos_shuttle_ctl).  The host
+// posts a descriptor with a few plain stores (no CUDA API call per chunk);
+// all CTAs copy their share of it over PCIe (zero-copy loads/stores of the
+// host slot), the last one to finish publishes done[slot] and, optionally, a
+// per-subgroup flag that a stream's cuStreamWaitValue32 is waiting on.
+// Because it is a running kernel, no stream's pending wait can ever sit in
+// front of its copies (streams share hardware queues; a wait at the head of
+// one blocks the others queued behind it — with host threads waiting on
+// those copies that deadlocks).
+namespace {
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_relaxed_sys64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_sys(const void* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+constexpr int kShuttleThreads = 512;
+
+__global__ void __launch_bounds__(kShuttleThreads) k_shuttle(dos_shuttle_ctl* ctl, uint32_t* flags,
+                                                              uint32_t* cnt, uint32_t first) {
+  __shared__ uint64_t s_src, s_dst;
+  __shared__ uint32_t s_bytes, s_flag_val;
+  __shared__ int32_t s_flag_idx;
+  __shared__ int s_quit;
+  const int tid = threadIdx.x, G = gridDim.x, me = blockIdx.x;
+  for (uint32_t k = first;; ++k) {
+    const uint32_t slot = k % DOS_SHUTTLE_Q;
+    dos_shuttle_desc* d = &ctl->q[slot];
+    if (tid == 0) {
+      s_quit = 0;
+      for (;;) {
+        if (ld_acquire_sys(&d->id) == k + 1) break;
+        if (ld_acquire_sys(&ctl->stop)) {  // descriptors are posted before stop: look once more
+          if (ld_acquire_sys(&d->id) != k + 1) s_quit = 1;
+          break;
+        }
+        __nanosleep(256);
+      }
+      if (!s_quit) {
+        s_src = ld_relaxed_sys64(&d->src);
+        s_dst = ld_relaxed_sys64(&d->dst);
+        s_bytes = ld_relaxed_sys(&d->bytes);
+        s_flag_idx = (int32_t)ld_relaxed_sys(&d->flag_idx);
+        s_flag_val = ld_relaxed_sys(&d->flag_val);
+      }
+    }
+    __syncthreads();
+    if (s_quit) return;
+    const char* src = reinterpret_cast<const char*>(s_src);
+    char* dst = reinterpret_cast<char*>(s_dst);
+    const uint32_t bytes = s_bytes;
+    if (((s_src | s_dst) & 15u) == 0) {
+      // 16-byte units, this CTA's contiguous share, 4 loads in flight per thread
+      const uint32_t units = bytes / 16, per = (units + G - 1) / G;
+      const uint32_t u0 = min(units, per * me), u1 = min(units, u0 + per);
+      const uint4* S = reinterpret_cast<const uint4*>(src);
+      uint4* D = reinterpret_cast<uint4*>(dst);
+      uint32_t u = u0 + tid;
+      for (; u + 3 * kShuttleThreads < u1; u += 4 * kShuttleThreads) {
+        const uint4 a = __ldcv(S + u), b = __ldcv(S + u + kShuttleThreads), c = __ldcv(S + u + 2 * kShuttleThreads),
+                    e = __ldcv(S + u + 3 * kShuttleThreads);
+        D[u] = a;
+        D[u + kShuttleThreads] = b;
+        D[u + 2 * kShuttleThreads] = c;
+        D[u + 3 * kShuttleThreads] = e;
+      }
+      for (; u < u1; u += kShuttleThreads) D[u] = __ldcv(S + u);
+      if (me == G - 1)  // tail bytes (16-bit elements)
+        for (uint32_t b = units * 16 + 2 * tid; b < bytes; b += 2 * kShuttleThreads)
+          *reinterpret_cast<uint16_t*>(dst + b) = __ldcv(reinterpret_cast<const unsigned short*>(src + b));
+    } else {  // unaligned: 16-bit elements
+      const uint32_t el = bytes / 2, per = (el + G - 1) / G;
+      const uint32_t e0 = min(el, per * me), e1 = min(el, e0 + per);
+      for (uint32_t e = e0 + tid; e < e1; e += kShuttleThreads)
+        reinterpret_cast<uint16_t*>(dst)[e] = __ldcv(reinterpret_cast<const unsigned short*>(src) + e);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence_system();  // this CTA's share is visible to the host and to every engine
+      if (atomicAdd(&cnt[slot], 1u) == (uint32_t)G - 1) {
+        __threadfence_system();
+        cnt[slot] = 0;
+        if (s_flag_idx >= 0) st_release_sys(&flags[s_flag_idx], s_flag_val);
+        st_release_sys(&ctl->done[slot], k + 1);
+      }
+    }
+    __syncthreads();
+  }
+}
+}  // namespace
+
+void dos_reserve_sms(int n) { g_reserved_sms.store(n < 0 ? 0 : n, std::memory_order_relaxed); }
+
+int dos_shuttle_launch(dos_shuttle_ctl* ctl_dev, uint32_t* flags_dev, uint32_t* cnt_dev, uint32_t first, int nctas,
+                       cudaStream_t st) {
+  k_shuttle<<<nctas, kShuttleThreads, 0, st>>>(ctl_dev, flags_dev, cnt_dev, first);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return dos_set_error(DOS_ECUDA, "shuttle launch failed: %s", cudaGetErrorString(e));
   return DOS_OK;
 }

@@ -93,18 +93,27 @@ struct Engine {
   cudaStream_t gst = nullptr;                        // in-phase grad flush (D2H); host_io: residents' grads H2D
   cudaStream_t ost = nullptr;                        // host_io: residents' working copy D2H
   cudaStream_t pst = nullptr;                        // fused all-gather: host subgroups' peer forwards
-  cudaStream_t wst = nullptr;                        // staging ring: working-copy chunks H2D
-  // staging ring (see RingCfg); ring_phase: used in this phase
+  cudaStream_t wst = nullptr;                        // the shuttle kernel's stream
+  // staging ring (see RingCfg) served by the shuttle kernel; ring_phase: used in this phase
   bool ring_phase = false;
   uint16_t* ring_mem = nullptr;
-  std::vector<cudaEvent_t> ring_ev;                   // per slot: its last shipped chunk has left the host
-  std::vector<uint8_t> ring_ev_live;
+  uint16_t* ring_mem_dev = nullptr;                   // its device alias (the shuttle reads it over PCIe)
+  std::vector<int64_t> ring_last;                     // per slot: shuttle descriptor that last shipped it (-1: none)
   int64_t ring_next = 0;                              // chunks shipped so far (the ring runs on across subgroups)
-  int64_t ring_sg_start = 0;                          // subgroup being shipped
+  int64_t ring_sg_start = 0, ring_sg_n = 0;           // subgroup being shipped
+  int ring_sg = -1;
   uint32_t* ring_flags = nullptr;                     // mapped: per subgroup, epoch once its last chunk landed
   CUdeviceptr ring_flags_dev = 0;
   int32_t ring_flags_cap = 0;
   pfn_write_value32 write_fn = nullptr;
+  // the shuttle: descriptor queue in mapped pinned memory + per-slot CTA counters in HBM
+  dos_shuttle_ctl* sh_ctl = nullptr;
+  dos_shuttle_ctl* sh_ctl_dev = nullptr;
+  uint32_t* sh_cnt = nullptr;
+  uint32_t sh_next = 0;        // next descriptor number (monotonic across phases)
+  uint32_t sh_phase_first = 0;  // first descriptor number of the running shuttle
+  bool sh_running = false;
+  int sh_ctas = 4;
   std::vector<cudaEvent_t> ev_g;                      // per action: its grads are on the host
   std::vector<cudaEvent_t> ev_sg;                     // per subgroup: host_io grads of a static resident landed
   std::deque<int32_t> static_q;                       // host_io_ahead: resident updates whose grads are in flight
@@ -217,21 +226,74 @@ struct Engine {
     }
   }
 
-  // staging-ring callbacks (run on the host worker = team thread 0)
+  // ---- shuttle queue (host side; only the host worker posts)
+  static void spin_pause(int i) {
+    if (i < 512) __builtin_ia32_pause();
+    else std::this_thread::yield();
+  }
+  bool sh_done(uint32_t id) const {
+    const uint32_t d = __atomic_load_n(&sh_ctl->done[id % DOS_SHUTTLE_Q], __ATOMIC_ACQUIRE);
+    return (int32_t)(d - (id + 1)) >= 0;
+  }
+  int sh_wait(uint32_t id) {
+    for (int i = 0; !sh_done(id); ++i) {
+      spin_pause(i);
+      if ((i & 0xFFFF) == 0xFFFF) {  // a dead shuttle must not hang the host lane
+        const cudaError_t q = cudaStreamQuery(wst);
+        if (q == cudaSuccess) return dos_set_error(DOS_ESTATE, "shuttle exited before descriptor %u", id);
+        if (q != cudaErrorNotReady) return dos_set_error(DOS_ECUDA, "shuttle failed: %s", cudaGetErrorString(q));
+      }
+    }
+    return DOS_OK;
+  }
+  int sh_post(const void* src_dev, void* dst_dev, uint32_t bytes, int32_t flag_idx, uint32_t flag_val,
+              uint32_t* id_out) {
+    const uint32_t id = sh_next++;
+    // the queue slot's previous descriptor (same phase) must be done
+    if (id - sh_phase_first >= DOS_SHUTTLE_Q) {
+      const int rc = sh_wait(id - DOS_SHUTTLE_Q);
+      if (rc != DOS_OK) return rc;
+    }
+    dos_shuttle_desc& d = sh_ctl->q[id % DOS_SHUTTLE_Q];
+    d.src = (uint64_t)(uintptr_t)src_dev;
+    d.dst = (uint64_t)(uintptr_t)dst_dev;
+    d.bytes = bytes;
+    d.flag_idx = flag_idx;
+    d.flag_val = flag_val;
+    __atomic_store_n(&d.id, id + 1, __ATOMIC_RELEASE);  // publishes the fields (x86: store order)
+    *id_out = id;
+    return DOS_OK;
+  }
+
+  // staging-ring callbacks (run on the host worker = team thread 0): post a
+  // shuttle descriptor per chunk / wait until a slot's last one is served
   static int ring_ship(void* ctx, int64_t, int slot, int64_t off, int64_t cnt) {
     Engine* e = static_cast<Engine*>(ctx);
     const RingCfg& rc = ring_cfg();
     char* dst = static_cast<char*>(e->S.dev_lowp) + 2 * (e->ring_sg_start + off);
-    DOS_CU(cudaMemcpyAsync(dst, e->ring_mem + (int64_t)slot * rc.chunk, (size_t)cnt * 2, cudaMemcpyHostToDevice, e->wst));
-    DOS_CU(cudaEventRecord(e->ring_ev[slot], e->wst));
-    e->ring_ev_live[slot] = 1;
+    const bool last = off + cnt == e->ring_sg_n;  // the subgroup's working copy is complete with this chunk
+    uint32_t id = 0;
+    const int r = e->sh_post(e->ring_mem_dev + (int64_t)slot * rc.chunk, dst, (uint32_t)(2 * cnt),
+                             last ? e->ring_sg : -1, e->epoch, &id);
+    if (r != DOS_OK) return r;
+    e->ring_last[slot] = id;
     return DOS_OK;
   }
   static int ring_reclaim(void* ctx, int slot) {
     Engine* e = static_cast<Engine*>(ctx);
-    if (e->ring_ev_live[slot]) DOS_CU(cudaEventSynchronize(e->ring_ev[slot]));
-    e->ring_ev_live[slot] = 0;
+    if (e->ring_last[slot] >= 0) {
+      const int r = e->sh_wait((uint32_t)e->ring_last[slot]);
+      if (r != DOS_OK) return r;
+    }
+    e->ring_last[slot] = -1;
     return DOS_OK;
+  }
+
+  // the shuttle runs for the whole phase: stop it once everything is posted
+  void sh_stop() {
+    if (!sh_running) return;
+    __atomic_store_n(&sh_ctl->stop, 1u, __ATOMIC_RELEASE);
+    sh_running = false;
   }
 
   int run_host(const Job& j, std::string& msg) {
@@ -243,11 +305,11 @@ struct Engine {
       const RingCfg& rc = ring_cfg();
       dos_ring r{ring_mem, rc.slots, rc.chunk, ring_next, this, ring_ship, ring_reclaim};
       ring_sg_start = a;
-      int code = dos_host_adam_ring(S.host_p + a, S.host_m + a, S.host_v + a, static_cast<const char*>(S.host_g) + 2 * a,
-                                    lt, lt, n, K, host_threads, r);
+      ring_sg_n = n;
+      ring_sg = j.sg;
+      const int code = dos_host_adam_ring(S.host_p + a, S.host_m + a, S.host_v + a,
+                                          static_cast<const char*>(S.host_g) + 2 * a, lt, lt, n, K, host_threads, r);
       ring_next += (n + rc.chunk - 1) / rc.chunk;
-      if (code == DOS_OK && write_fn(( CUstream)wst, ring_flags_dev + 4 * (CUdeviceptr)j.sg, epoch, 0) != CUDA_SUCCESS)
-        code = dos_set_error(DOS_ECUDA, "cuStreamWriteValue32 (staging ring) failed");
       if (code != DOS_OK) msg = dos_last_error();
       return code;
     }
@@ -517,6 +579,11 @@ struct Engine {
       return dos_set_error(DOS_ETYPE, "working-copy dtype %d unsupported", st_desc->lowp_dtype);
     if (nmax < 0) return dos_set_error(DOS_EINVAL, "max_actions must be >= 0");
     DOS_CU(cudaSetDevice(dev));
+    if (sh_running) {  // a shuttle left over by a begin() that failed after launching it
+      sh_stop();
+      cudaStreamSynchronize(wst);
+      dos_reserve_sms(0);
+    }
     S = *st_desc;
     const int ns = S.num_subgroups;
     sg_start.assign(S.sg_start, S.sg_start + ns);
@@ -590,13 +657,34 @@ struct Engine {
     // the staging ring carries the working copy of host-updated subgroups in
     // the device-resident mode with the downscale fused (host_io mirrors the
     // working copy into the host image instead)
-    ring_phase = ring_cfg().on && fuse && !S.host_io && wait_fn && write_fn && wait_value_ok;
+    ring_phase = ring_cfg().on && fuse && !S.host_io && S.host_updates != 0 && wait_fn && wait_value_ok;
     if (ring_phase && !ring_mem) {
       const RingCfg& rc = ring_cfg();
-      DOS_CU(cudaHostAlloc(reinterpret_cast<void**>(&ring_mem), (size_t)rc.slots * rc.chunk * 2, cudaHostAllocDefault));
-      ring_ev.resize(rc.slots);
-      ring_ev_live.assign(rc.slots, 0);
-      for (auto& e : ring_ev) DOS_CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      DOS_CU(cudaHostAlloc(reinterpret_cast<void**>(&ring_mem), (size_t)rc.slots * rc.chunk * 2, cudaHostAllocMapped));
+      void* dptr = nullptr;
+      DOS_CU(cudaHostGetDevicePointer(&dptr, ring_mem, 0));
+      ring_mem_dev = static_cast<uint16_t*>(dptr);
+      ring_last.assign(rc.slots, -1);
+      DOS_CU(cudaHostAlloc(reinterpret_cast<void**>(&sh_ctl), sizeof(dos_shuttle_ctl), cudaHostAllocMapped));
+      memset(sh_ctl, 0, sizeof(dos_shuttle_ctl));
+      DOS_CU(cudaHostGetDevicePointer(&dptr, sh_ctl, 0));
+      sh_ctl_dev = static_cast<dos_shuttle_ctl*>(dptr);
+      DOS_CU(cudaMalloc(reinterpret_cast<void**>(&sh_cnt), DOS_SHUTTLE_Q * 4));
+      DOS_CU(cudaMemset(sh_cnt, 0, DOS_SHUTTLE_Q * 4));
+      DOS_CU(cudaDeviceSynchronize());
+      if (const char* e = getenv("DOS_SHUTTLE_CTAS")) sh_ctas = std::max(1, std::min(32, atoi(e)));
+    }
+    if (ring_phase) {
+      // launched before anything of this phase is queued anywhere: no stream's
+      // pending wait can sit in front of it
+      std::fill(ring_last.begin(), ring_last.end(), -1);
+      __atomic_store_n(&sh_ctl->stop, 0u, __ATOMIC_RELEASE);
+      sh_phase_first = sh_next;
+      const int rc = dos_shuttle_launch(sh_ctl_dev, reinterpret_cast<uint32_t*>(ring_flags_dev), sh_cnt, sh_next,
+                                        sh_ctas, wst);
+      if (rc != DOS_OK) return rc;
+      sh_running = true;
+      dos_reserve_sms(sh_ctas);
     }
     max_actions = cap;
     count = 0;
@@ -619,7 +707,6 @@ struct Engine {
     DOS_CU(cudaStreamWaitEvent(gst, ev0, 0));
     DOS_CU(cudaStreamWaitEvent(ost, ev0, 0));
     DOS_CU(cudaStreamWaitEvent(pst, ev0, 0));
-    DOS_CU(cudaStreamWaitEvent(wst, ev0, 0));
     flush_q.clear();
     if (S.host_io) {
       // static residents' grads go H2D first thing, on the side stream, so
@@ -648,12 +735,14 @@ struct Engine {
       std::unique_lock<std::mutex> lk(mu);
       done_cv.wait(lk, [&] { return inflight == 0; });
     }
+    sh_stop();  // the host lane posted everything: the shuttle drains and exits
     active = false;
     cudaError_t ce = cudaSuccess;
     for (int i = 0; i < 7; ++i) {
       cudaError_t e = cudaStreamSynchronize(i < 3 ? st[i] : i == 3 ? gst : i == 4 ? ost : i == 5 ? pst : wst);
       if (e != cudaSuccess && ce == cudaSuccess) ce = e;
     }
+    dos_reserve_sms(0);
     if (ce != cudaSuccess) return dos_set_error(DOS_ECUDA, "update phase failed on the device: %s", cudaGetErrorString(ce));
     if (host_err != DOS_OK) return dos_set_error(host_err, "host lane: %s", host_errmsg.c_str());
     if (err != DOS_OK) return dos_set_error(err, "%s", errmsg.c_str());
@@ -710,6 +799,7 @@ struct Engine {
   }
 
   void destroy() {
+    if (sh_ctl) sh_stop();
     {
       std::lock_guard<std::mutex> lk(mu);
       stop = true;
@@ -735,8 +825,9 @@ struct Engine {
     if (slot_mem) cudaFree(slot_mem);
     if (flags) cudaFreeHost(flags);
     if (ring_flags) cudaFreeHost(ring_flags);
-    for (auto e : ring_ev) cudaEventDestroy(e);
     if (ring_mem) cudaFreeHost(ring_mem);
+    if (sh_ctl) cudaFreeHost(sh_ctl);
+    if (sh_cnt) cudaFree(sh_cnt);
   }
 };
 

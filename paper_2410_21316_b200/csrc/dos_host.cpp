@@ -220,7 +220,12 @@ class SpinBarrier {
       gen_.store(g + 1, std::memory_order_release);
       return;
     }
-    while (gen_.load(std::memory_order_acquire) == g) __builtin_ia32_pause();
+    // spin briefly, then yield: the caller (thread 0) is not pinned and may
+    // share a core with a spinning worker, which must then give the core up
+    for (int i = 0; gen_.load(std::memory_order_acquire) == g; ++i) {
+      if (i < 256) __builtin_ia32_pause();
+      else sched_yield();
+    }
   }
 
  private:

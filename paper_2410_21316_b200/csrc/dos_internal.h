@@ -83,3 +83,24 @@ int dos_host_adam_ring(float* p, float* m, float* v, const void* g, int gt, int 
 extern const dos_hk_table dos_hk_avx512;
 extern const dos_hk_table dos_hk_avx2;
 extern const dos_hk_table dos_hk_generic;
+
+// The shuttle (dos_cuda.cu): a persistent kernel serving copy descriptors
+// posted by the host lane into mapped pinned memory (see k_shuttle).
+#define DOS_SHUTTLE_Q 256
+struct dos_shuttle_desc {  // 32 B; `id` (= descriptor number + 1) is written last
+  uint64_t src, dst;       // device-accessible addresses (host memory: its device alias)
+  uint32_t bytes;
+  int32_t flag_idx;        // >= 0: flags[flag_idx] = flag_val once the copy has landed
+  uint32_t flag_val;
+  uint32_t id;
+};
+struct dos_shuttle_ctl {
+  uint32_t stop;           // host: every descriptor of the phase is posted; exit when drained
+  uint32_t pad[31];
+  uint32_t done[DOS_SHUTTLE_Q];  // kernel: descriptor number + 1 of the last completed one per queue slot
+  dos_shuttle_desc q[DOS_SHUTTLE_Q];
+};
+int dos_shuttle_launch(dos_shuttle_ctl* ctl_dev, uint32_t* flags_dev, uint32_t* cnt_dev, uint32_t first, int nctas,
+                       cudaStream_t st);
+// SMs kept free of K1's persistent grid while a shuttle runs.
+void dos_reserve_sms(int n);

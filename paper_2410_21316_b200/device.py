@@ -289,7 +289,8 @@ class DeviceResidency:
         return eng
 
     def state_desc(self, host_io: bool = False, peers=None, flush_grads: bool = False,
-                   grad_sources=None, host_io_ahead: int = 0) -> tuple[N.dos_state_desc, list]:
+                   grad_sources=None, host_io_ahead: int = 0,
+                   host_updates: int = -1) -> tuple[N.dos_state_desc, list]:
         """``peers``: addresses (ints) where this shard starts in each peer's
         full-model buffer — the fused all-gather targets (include/dos.h).
         ``grad_sources``: a ``distributed.GradSources`` (fused reduce-scatter)."""
@@ -316,6 +317,7 @@ class DeviceResidency:
             dev_static_p=None, dev_static_m=None, dev_static_v=None,
             dev_static_sg=C.cast(self._static_ptrs, C.POINTER(C.c_void_p)),
             host_io_ahead=host_io_ahead,
+            host_updates=host_updates,
             host_io=1 if host_io else 0,
             npeers=len(peers),
             peer_lowp=C.cast(peer_arr, C.POINTER(C.c_void_p)),
@@ -448,7 +450,9 @@ class B200Target(SimTarget):
         # just ahead of it; residents that trail it get them all at phase start
         first_fast = next((a.subgroup for a in self.plan.actions if a.kind.value == "gpu_update"), None)
         ahead = 2 if (self.host_io and first_fast is not None and first_fast in self.plan.static_set) else 0
-        desc, keep = self.residency.state_desc(self.host_io, self.peers, self.flush_grads, self.grad_sources, ahead)
+        host_updates = sum(1 for a in self.plan.actions if a.kind.value == "cpu_update")
+        desc, keep = self.residency.state_desc(self.host_io, self.peers, self.flush_grads, self.grad_sources, ahead,
+                                               host_updates)
         self._keep = (desc, keep)
         h = self.hyper
         bc1, bc2 = bias_corrections(h.beta1, h.beta2, self.step)

@@ -1,5 +1,5 @@
 """The host lane's working-copy staging ring (dos_host_adam_ring + the
-engine's ring stream): host-updated subgroups' working copy goes H2D in
+shuttle kernel): host-updated subgroups' working copy goes H2D in
 LLC-resident chunks during the CPU update instead of through the host image.
 Bit-exact against the oracle with many chunks per subgroup, ragged chunks,
 two-slot wrap-around across subgroups, every plan shape, and with the ring
@@ -48,10 +48,16 @@ print("ring ok")
 @pytest.mark.parametrize("env", [
     {},  # default ring (4 x 512K: one chunk per small subgroup)
     {"DOS_W_RING_CHUNK": "4096", "DOS_W_RING_SLOTS": "2"},  # many ragged chunks, tight wrap-around
-    {"DOS_W_RING_CHUNK": "12288", "DOS_W_RING_SLOTS": "3"},
+    {"DOS_W_RING_CHUNK": "12288", "DOS_W_RING_SLOTS": "3", "DOS_SHUTTLE_CTAS": "1"},
+    # every stream on ONE hardware queue: a wait at the head of any stream blocks
+    # all the others queued behind it.  The engine must still finish: every
+    # GPU-side wait is on a host action emitted earlier, and the ring's copies
+    # are served by a kernel launched before anything else of the phase
+    {"CUDA_DEVICE_MAX_CONNECTIONS": "1", "DOS_W_RING_CHUNK": "12288", "DOS_W_RING_SLOTS": "3"},
+    {"CUDA_DEVICE_MAX_CONNECTIONS": "1", "DOS_W_RING": "0"},
     {"DOS_W_RING": "0"},  # off: H1 -> host image -> H2D_PARAMS16
 ])
 def test_ring_bit_exact(env):
     proc = subprocess.run([sys.executable, "-c", CHECK], cwd=ROOT, env=dict(os.environ, **env), capture_output=True,
-                          text=True, timeout=900)
+                          text=True, timeout=600)
     assert proc.returncode == 0 and "ring ok" in proc.stdout, proc.stdout[-2000:] + proc.stderr[-3000:]
