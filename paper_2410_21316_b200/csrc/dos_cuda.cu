@@ -1089,11 +1089,11 @@ extern "C" int dos_coherence_cuda(const dos_coh_range* ranges, int nranges, int 
 // ---------------------------------------------------------------- shuttle
 // The host lane's copy engine for small, LLC-resident staging slots: a
 // persistent kernel of a few CTAs, launched at phase start, that serves a
-// descriptor queue in mapped pinned host memory (dos_shuttle_ctl).  The host
-// posts a descriptor with a few plain stores (no CUDA API call per chunk);
-// all CTAs copy their share of it over PCIe (zero-copy loads/stores of the
-// host slot), the last one to finish publishes done[slot] and, optionally, a
-// per-subgroup flag that a stream's cuStreamWaitValue32 is waiting on.
+// descriptor queue in mapped pinned host memory (dos_shuttle_ctl).  Host
+// threads post descriptors with a few plain stores (no CUDA API call per
+// chunk); each descriptor is copied over PCIe (zero-copy loads of the host
+// slot) by one CTA, which then publishes done[slot] and, optionally, a flag
+// that a stream's cuStreamWaitValue32 is waiting on.
 // Because it is a running kernel, no stream's pending wait can ever sit in
 // front of its copies (streams share hardware queues; a wait at the head of
 // one blocks the others queued behind it — with host threads waiting on
@@ -1120,25 +1120,27 @@ __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
 
 constexpr int kShuttleThreads = 512;
 
-__global__ void __launch_bounds__(kShuttleThreads) k_shuttle(dos_shuttle_ctl* ctl, uint32_t* flags,
-                                                              uint32_t* cnt, uint32_t first) {
+// CTA `me` serves descriptors first + me, first + me + G, ... on its own (a
+// descriptor is a whole staging slot, copied by the CTA's threads with 4 PCIe
+// loads in flight each), so the CTAs never wait for each other.
+__global__ void __launch_bounds__(kShuttleThreads) k_shuttle(dos_shuttle_ctl* ctl, uint32_t* flags, uint32_t first) {
   __shared__ uint64_t s_src, s_dst;
   __shared__ uint32_t s_bytes, s_flag_val;
   __shared__ int32_t s_flag_idx;
   __shared__ int s_quit;
-  const int tid = threadIdx.x, G = gridDim.x, me = blockIdx.x;
-  for (uint32_t k = first;; ++k) {
+  const int tid = threadIdx.x;
+  for (uint32_t k = first + blockIdx.x;; k += gridDim.x) {
     const uint32_t slot = k % DOS_SHUTTLE_Q;
     dos_shuttle_desc* d = &ctl->q[slot];
     if (tid == 0) {
       s_quit = 0;
       for (;;) {
         if (ld_acquire_sys(&d->id) == k + 1) break;
-        if (ld_acquire_sys(&ctl->stop)) {  // descriptors are posted before stop: look once more
+        if (ld_acquire_sys(&ctl->stop)) {  // every descriptor is posted before stop: look once more
           if (ld_acquire_sys(&d->id) != k + 1) s_quit = 1;
           break;
         }
-        __nanosleep(256);
+        __nanosleep(128);
       }
       if (!s_quit) {
         s_src = ld_relaxed_sys64(&d->src);
@@ -1154,13 +1156,11 @@ __global__ void __launch_bounds__(kShuttleThreads) k_shuttle(dos_shuttle_ctl* ct
     char* dst = reinterpret_cast<char*>(s_dst);
     const uint32_t bytes = s_bytes;
     if (((s_src | s_dst) & 15u) == 0) {
-      // 16-byte units, this CTA's contiguous share, 4 loads in flight per thread
-      const uint32_t units = bytes / 16, per = (units + G - 1) / G;
-      const uint32_t u0 = min(units, per * me), u1 = min(units, u0 + per);
+      const uint32_t units = bytes / 16;
       const uint4* S = reinterpret_cast<const uint4*>(src);
       uint4* D = reinterpret_cast<uint4*>(dst);
-      uint32_t u = u0 + tid;
-      for (; u + 3 * kShuttleThreads < u1; u += 4 * kShuttleThreads) {
+      uint32_t u = tid;
+      for (; u + 3 * kShuttleThreads < units; u += 4 * kShuttleThreads) {
         const uint4 a = __ldcv(S + u), b = __ldcv(S + u + kShuttleThreads), c = __ldcv(S + u + 2 * kShuttleThreads),
                     e = __ldcv(S + u + 3 * kShuttleThreads);
         D[u] = a;
@@ -1168,36 +1168,27 @@ __global__ void __launch_bounds__(kShuttleThreads) k_shuttle(dos_shuttle_ctl* ct
         D[u + 2 * kShuttleThreads] = c;
         D[u + 3 * kShuttleThreads] = e;
       }
-      for (; u < u1; u += kShuttleThreads) D[u] = __ldcv(S + u);
-      if (me == G - 1)  // tail bytes (16-bit elements)
-        for (uint32_t b = units * 16 + 2 * tid; b < bytes; b += 2 * kShuttleThreads)
-          *reinterpret_cast<uint16_t*>(dst + b) = __ldcv(reinterpret_cast<const unsigned short*>(src + b));
+      for (; u < units; u += kShuttleThreads) D[u] = __ldcv(S + u);
+      for (uint32_t b = units * 16 + 2 * tid; b < bytes; b += 2 * kShuttleThreads)  // tail (16-bit elements)
+        *reinterpret_cast<uint16_t*>(dst + b) = __ldcv(reinterpret_cast<const unsigned short*>(src + b));
     } else {  // unaligned: 16-bit elements
-      const uint32_t el = bytes / 2, per = (el + G - 1) / G;
-      const uint32_t e0 = min(el, per * me), e1 = min(el, e0 + per);
-      for (uint32_t e = e0 + tid; e < e1; e += kShuttleThreads)
+      for (uint32_t e = tid; e < bytes / 2; e += kShuttleThreads)
         reinterpret_cast<uint16_t*>(dst)[e] = __ldcv(reinterpret_cast<const unsigned short*>(src) + e);
     }
     __syncthreads();
     if (tid == 0) {
-      __threadfence_system();  // this CTA's share is visible to the host and to every engine
-      if (atomicAdd(&cnt[slot], 1u) == (uint32_t)G - 1) {
-        __threadfence_system();
-        cnt[slot] = 0;
-        if (s_flag_idx >= 0) st_release_sys(&flags[s_flag_idx], s_flag_val);
-        st_release_sys(&ctl->done[slot], k + 1);
-      }
+      __threadfence_system();  // the copy is visible to the host and to every engine
+      if (s_flag_idx >= 0) st_release_sys(&flags[s_flag_idx], s_flag_val);
+      st_release_sys(&ctl->done[slot], k + 1);
     }
-    __syncthreads();
   }
 }
 }  // namespace
 
 void dos_reserve_sms(int n) { g_reserved_sms.store(n < 0 ? 0 : n, std::memory_order_relaxed); }
 
-int dos_shuttle_launch(dos_shuttle_ctl* ctl_dev, uint32_t* flags_dev, uint32_t* cnt_dev, uint32_t first, int nctas,
-                       cudaStream_t st) {
-  k_shuttle<<<nctas, kShuttleThreads, 0, st>>>(ctl_dev, flags_dev, cnt_dev, first);
+int dos_shuttle_launch(dos_shuttle_ctl* ctl_dev, uint32_t* flags_dev, uint32_t first, int nctas, cudaStream_t st) {
+  k_shuttle<<<nctas, kShuttleThreads, 0, st>>>(ctl_dev, flags_dev, first);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return dos_set_error(DOS_ECUDA, "shuttle launch failed: %s", cudaGetErrorString(e));

@@ -54,15 +54,17 @@ typedef CUresult (*pfn_write_value32)(CUstream, CUdeviceptr, cuuint32_t, unsigne
 // image with non-temporal stores and H2D_PARAMS16 ships it from there).
 struct RingCfg {
   bool on;
-  int slots;
-  int64_t chunk;
+  int slots;      // per team thread
+  int64_t chunk;  // elements per slot
+  int ctas;       // shuttle CTAs
 };
 const RingCfg& ring_cfg() {
   static RingCfg c = [] {
-    RingCfg r{true, 4, 1 << 19};  // 4 x 512K elements (4 MB of bf16)
+    RingCfg r{true, 4, 1 << 16, 8};  // per thread 4 x 64K elements (512 KB of bf16: the core's L2)
     if (const char* e = getenv("DOS_W_RING")) r.on = strcmp(e, "0") != 0;
-    if (const char* e = getenv("DOS_W_RING_SLOTS")) r.slots = std::max(2, std::min(64, atoi(e)));
-    if (const char* e = getenv("DOS_W_RING_CHUNK")) r.chunk = std::max<int64_t>(4096, atoll(e)) & ~int64_t(63);
+    if (const char* e = getenv("DOS_W_RING_SLOTS")) r.slots = std::max(1, std::min(64, atoi(e)));
+    if (const char* e = getenv("DOS_W_RING_CHUNK")) r.chunk = std::max<int64_t>(1024, atoll(e)) & ~int64_t(63);
+    if (const char* e = getenv("DOS_SHUTTLE_CTAS")) r.ctas = std::max(1, std::min(32, atoi(e)));
     return r;
   }();
   return c;
@@ -98,22 +100,19 @@ struct Engine {
   bool ring_phase = false;
   uint16_t* ring_mem = nullptr;
   uint16_t* ring_mem_dev = nullptr;                   // its device alias (the shuttle reads it over PCIe)
-  std::vector<int64_t> ring_last;                     // per slot: shuttle descriptor that last shipped it (-1: none)
-  int64_t ring_next = 0;                              // chunks shipped so far (the ring runs on across subgroups)
-  int64_t ring_sg_start = 0, ring_sg_n = 0;           // subgroup being shipped
-  int ring_sg = -1;
+  int ring_threads = 0;                               // team threads the slots are laid out for
+  std::vector<int64_t> ring_last;                     // per thread slot: its last shuttle descriptor (-1: none)
+  int64_t ring_sg_start = 0;                          // subgroup being shipped
   uint32_t* ring_flags = nullptr;                     // mapped: per subgroup, epoch once its last chunk landed
   CUdeviceptr ring_flags_dev = 0;
   int32_t ring_flags_cap = 0;
   pfn_write_value32 write_fn = nullptr;
-  // the shuttle: descriptor queue in mapped pinned memory + per-slot CTA counters in HBM
+  // the shuttle: descriptor queue in mapped pinned memory
   dos_shuttle_ctl* sh_ctl = nullptr;
   dos_shuttle_ctl* sh_ctl_dev = nullptr;
-  uint32_t* sh_cnt = nullptr;
-  uint32_t sh_next = 0;        // next descriptor number (monotonic across phases)
-  uint32_t sh_phase_first = 0;  // first descriptor number of the running shuttle
+  std::atomic<uint32_t> sh_next{0};  // next descriptor number (monotonic across phases; posted by many threads)
+  uint32_t sh_phase_first = 0;       // first descriptor number of the running shuttle
   bool sh_running = false;
-  int sh_ctas = 4;
   std::vector<cudaEvent_t> ev_g;                      // per action: its grads are on the host
   std::vector<cudaEvent_t> ev_sg;                     // per subgroup: host_io grads of a static resident landed
   std::deque<int32_t> static_q;                       // host_io_ahead: resident updates whose grads are in flight
@@ -246,9 +245,10 @@ struct Engine {
     }
     return DOS_OK;
   }
-  int sh_post(const void* src_dev, void* dst_dev, uint32_t bytes, int32_t flag_idx, uint32_t flag_val,
-              uint32_t* id_out) {
-    const uint32_t id = sh_next++;
+  // any team thread may post (the queue is multi-producer: numbers are
+  // claimed atomically, each descriptor is published by its own id store)
+  int64_t sh_post(const void* src_dev, void* dst_dev, uint32_t bytes, int32_t flag_idx, uint32_t flag_val) {
+    const uint32_t id = sh_next.fetch_add(1, std::memory_order_relaxed);
     // the queue slot's previous descriptor (same phase) must be done
     if (id - sh_phase_first >= DOS_SHUTTLE_Q) {
       const int rc = sh_wait(id - DOS_SHUTTLE_Q);
@@ -261,33 +261,16 @@ struct Engine {
     d.flag_idx = flag_idx;
     d.flag_val = flag_val;
     __atomic_store_n(&d.id, id + 1, __ATOMIC_RELEASE);  // publishes the fields (x86: store order)
-    *id_out = id;
-    return DOS_OK;
+    return id;
   }
 
-  // staging-ring callbacks (run on the host worker = team thread 0): post a
-  // shuttle descriptor per chunk / wait until a slot's last one is served
-  static int ring_ship(void* ctx, int64_t, int slot, int64_t off, int64_t cnt) {
+  // staging-ring callbacks (run on every team thread)
+  static int64_t ring_post(void* ctx, const uint16_t* slot, int64_t off, int64_t cnt) {
     Engine* e = static_cast<Engine*>(ctx);
-    const RingCfg& rc = ring_cfg();
     char* dst = static_cast<char*>(e->S.dev_lowp) + 2 * (e->ring_sg_start + off);
-    const bool last = off + cnt == e->ring_sg_n;  // the subgroup's working copy is complete with this chunk
-    uint32_t id = 0;
-    const int r = e->sh_post(e->ring_mem_dev + (int64_t)slot * rc.chunk, dst, (uint32_t)(2 * cnt),
-                             last ? e->ring_sg : -1, e->epoch, &id);
-    if (r != DOS_OK) return r;
-    e->ring_last[slot] = id;
-    return DOS_OK;
+    return e->sh_post(e->ring_mem_dev + (slot - e->ring_mem), dst, (uint32_t)(2 * cnt), -1, 0);
   }
-  static int ring_reclaim(void* ctx, int slot) {
-    Engine* e = static_cast<Engine*>(ctx);
-    if (e->ring_last[slot] >= 0) {
-      const int r = e->sh_wait((uint32_t)e->ring_last[slot]);
-      if (r != DOS_OK) return r;
-    }
-    e->ring_last[slot] = -1;
-    return DOS_OK;
-  }
+  static int ring_wait(void* ctx, int64_t id) { return static_cast<Engine*>(ctx)->sh_wait((uint32_t)id); }
 
   // the shuttle runs for the whole phase: stop it once everything is posted
   void sh_stop() {
@@ -299,17 +282,20 @@ struct Engine {
   int run_host(const Job& j, std::string& msg) {
     const int lt = S.lowp_dtype;
     if (j.kind == DOS_CPU_UPDATE && ring_phase) {
-      // the working copy leaves through the LLC-resident staging ring; its
-      // last chunk's landing is published per subgroup for H2D_PARAMS16
+      // the working copy leaves through the team's LLC-resident staging
+      // slots, served by the shuttle; once every chunk has landed the
+      // subgroup's flag releases its H2D_PARAMS16
       const int64_t a = sg_start[j.sg], n = sg_size[j.sg];
       const RingCfg& rc = ring_cfg();
-      dos_ring r{ring_mem, rc.slots, rc.chunk, ring_next, this, ring_ship, ring_reclaim};
+      std::fill(ring_last.begin(), ring_last.end(), -1);
+      dos_ring r{ring_mem, ring_threads, rc.slots, rc.chunk, this, ring_post, ring_wait};
       ring_sg_start = a;
-      ring_sg_n = n;
-      ring_sg = j.sg;
-      const int code = dos_host_adam_ring(S.host_p + a, S.host_m + a, S.host_v + a,
-                                          static_cast<const char*>(S.host_g) + 2 * a, lt, lt, n, K, host_threads, r);
-      ring_next += (n + rc.chunk - 1) / rc.chunk;
+      int code = dos_host_adam_ring(S.host_p + a, S.host_m + a, S.host_v + a,
+                                    static_cast<const char*>(S.host_g) + 2 * a, lt, lt, n, K, host_threads, r,
+                                    ring_last.data());
+      for (int64_t id : ring_last)
+        if (code == DOS_OK && id >= 0) code = sh_wait((uint32_t)id);
+      if (code == DOS_OK) __atomic_store_n(&ring_flags[j.sg], epoch, __ATOMIC_RELEASE);
       if (code != DOS_OK) msg = dos_last_error();
       return code;
     }
@@ -658,33 +644,35 @@ struct Engine {
     // the device-resident mode with the downscale fused (host_io mirrors the
     // working copy into the host image instead)
     ring_phase = ring_cfg().on && fuse && !S.host_io && S.host_updates != 0 && wait_fn && wait_value_ok;
-    if (ring_phase && !ring_mem) {
+    if (ring_phase && (!ring_mem || ring_threads < dos_host_threads())) {
       const RingCfg& rc = ring_cfg();
-      DOS_CU(cudaHostAlloc(reinterpret_cast<void**>(&ring_mem), (size_t)rc.slots * rc.chunk * 2, cudaHostAllocMapped));
+      if (ring_mem) cudaFreeHost(ring_mem);
+      ring_threads = dos_host_threads();
+      const size_t bytes = (size_t)ring_threads * rc.slots * rc.chunk * 2;
+      DOS_CU(cudaHostAlloc(reinterpret_cast<void**>(&ring_mem), bytes, cudaHostAllocMapped));
       void* dptr = nullptr;
       DOS_CU(cudaHostGetDevicePointer(&dptr, ring_mem, 0));
       ring_mem_dev = static_cast<uint16_t*>(dptr);
-      ring_last.assign(rc.slots, -1);
+      ring_last.assign((size_t)ring_threads * rc.slots, -1);
+    }
+    if (ring_phase && !sh_ctl) {
       DOS_CU(cudaHostAlloc(reinterpret_cast<void**>(&sh_ctl), sizeof(dos_shuttle_ctl), cudaHostAllocMapped));
       memset(sh_ctl, 0, sizeof(dos_shuttle_ctl));
+      void* dptr = nullptr;
       DOS_CU(cudaHostGetDevicePointer(&dptr, sh_ctl, 0));
       sh_ctl_dev = static_cast<dos_shuttle_ctl*>(dptr);
-      DOS_CU(cudaMalloc(reinterpret_cast<void**>(&sh_cnt), DOS_SHUTTLE_Q * 4));
-      DOS_CU(cudaMemset(sh_cnt, 0, DOS_SHUTTLE_Q * 4));
-      DOS_CU(cudaDeviceSynchronize());
-      if (const char* e = getenv("DOS_SHUTTLE_CTAS")) sh_ctas = std::max(1, std::min(32, atoi(e)));
     }
     if (ring_phase) {
       // launched before anything of this phase is queued anywhere: no stream's
       // pending wait can sit in front of it
-      std::fill(ring_last.begin(), ring_last.end(), -1);
       __atomic_store_n(&sh_ctl->stop, 0u, __ATOMIC_RELEASE);
-      sh_phase_first = sh_next;
-      const int rc = dos_shuttle_launch(sh_ctl_dev, reinterpret_cast<uint32_t*>(ring_flags_dev), sh_cnt, sh_next,
-                                        sh_ctas, wst);
+      sh_phase_first = sh_next.load();
+      const int ctas = ring_cfg().ctas;
+      const int rc = dos_shuttle_launch(sh_ctl_dev, reinterpret_cast<uint32_t*>(ring_flags_dev), sh_phase_first, ctas,
+                                        wst);
       if (rc != DOS_OK) return rc;
       sh_running = true;
-      dos_reserve_sms(sh_ctas);
+      dos_reserve_sms(ctas);
     }
     max_actions = cap;
     count = 0;
@@ -827,7 +815,6 @@ struct Engine {
     if (ring_flags) cudaFreeHost(ring_flags);
     if (ring_mem) cudaFreeHost(ring_mem);
     if (sh_ctl) cudaFreeHost(sh_ctl);
-    if (sh_cnt) cudaFree(sh_cnt);
   }
 };
 

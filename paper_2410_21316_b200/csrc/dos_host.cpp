@@ -206,73 +206,44 @@ int dos_host_adam(float* p, float* m, float* v, const void* g, int gt, void* lp,
   return DOS_OK;
 }
 
-namespace {
-// Sense-reversing spin barrier for the k threads of one team job (the
-// per-chunk sync of the staging ring: ~1 us, where the team's own fork-join
-// would cost a condition-variable round trip per chunk).
-class SpinBarrier {
- public:
-  explicit SpinBarrier(int k) : k_(k) {}
-  void arrive_and_wait() {
-    const int g = gen_.load(std::memory_order_acquire);
-    if (count_.fetch_add(1, std::memory_order_acq_rel) == k_ - 1) {
-      count_.store(0, std::memory_order_relaxed);
-      gen_.store(g + 1, std::memory_order_release);
-      return;
-    }
-    // spin briefly, then yield: the caller (thread 0) is not pinned and may
-    // share a core with a spinning worker, which must then give the core up
-    for (int i = 0; gen_.load(std::memory_order_acquire) == g; ++i) {
-      if (i < 256) __builtin_ia32_pause();
-      else sched_yield();
-    }
-  }
-
- private:
-  const int k_;
-  std::atomic<int> count_{0};
-  std::atomic<int> gen_{0};
-};
-}  // namespace
-
 int dos_host_adam_ring(float* p, float* m, float* v, const void* g, int gt, int lt, int64_t n, const dos_kscal& s,
-                       int nthreads, const dos_ring& ring) {
+                       int nthreads, const dos_ring& ring, int64_t* last) {
   if (n == 0) return DOS_OK;
-  if (lt == DOS_NONE || ring.nslots < 2 || ring.chunk < 64 || !ring.slots || !ring.ship || !ring.reclaim)
+  if (lt == DOS_NONE || ring.nslots < 1 || ring.chunk < 64 || !ring.slots || !ring.post || !ring.wait || !last)
     return dos_set_error(DOS_EINVAL, "staging ring: bad configuration");
   const dos_hk_table& t = hk();
   const std::shared_ptr<Team> hold = team();
   Team& tm = *hold;
   int k = nthreads > 0 ? std::min(nthreads, tm.size()) : tm.size();
-  const int64_t nchunks = (n + ring.chunk - 1) / ring.chunk;
+  k = std::min(k, ring.nthreads);
   const int gsz = gt == DOS_F32 ? 4 : 2;
-  auto slot_of = [&](int64_t c) { return (int)((ring.first + c) % ring.nslots); };
-  // the slot of chunk 0 may still be shipping the previous subgroup's last chunks
-  const int rc0 = ring.reclaim(ring.ctx, slot_of(0));
-  if (rc0 != DOS_OK) return rc0;
-  SpinBarrier bar(k);
+  // contiguous, 64-element aligned slice per thread (as dos_host_adam)
+  const int64_t per = ((n + k - 1) / k + 63) & ~int64_t(63);
   std::atomic<int> err{DOS_OK};
   tm.run(k, [&](int tid) {
-    for (int64_t c = 0; c < nchunks; ++c) {
-      const int64_t c0 = c * ring.chunk, len = std::min(ring.chunk, n - c0);
-      const int slot = slot_of(c);
-      // this thread's slice of the chunk, 64-element aligned
-      const int64_t per = ((len + k - 1) / k + 63) & ~int64_t(63);
-      const int64_t lo = std::min<int64_t>(len, per * tid), hi = std::min<int64_t>(len, lo + per);
-      if (lo < hi)
-        t.adam_cached(p + c0, m + c0, v + c0, static_cast<const char*>(g) + gsz * c0, gt,
-                      ring.slots + (int64_t)slot * ring.chunk, lt, lo, hi, s);
-      if (tid == 0 && c + 1 < nchunks && err.load(std::memory_order_relaxed) == DOS_OK) {
-        // the slot chunk c + 1 writes must have left the host (its copy,
-        // shipped nslots - 1 chunks ago) before anyone starts chunk c + 1
-        const int rc = ring.reclaim(ring.ctx, slot_of(c + 1));
-        if (rc != DOS_OK) err.store(rc);
+    const int64_t lo = std::min<int64_t>(n, per * tid), hi = std::min<int64_t>(n, lo + per);
+    int64_t* mine = last + (int64_t)tid * ring.nslots;
+    uint16_t* base = ring.slots + (int64_t)tid * ring.nslots * ring.chunk;
+    int slot = 0;
+    for (int64_t c0 = lo; c0 < hi; c0 += ring.chunk) {
+      const int64_t len = std::min(ring.chunk, hi - c0);
+      if (mine[slot] >= 0) {  // the slot's previous chunk must have left the host
+        const int rc = ring.wait(ring.ctx, mine[slot]);
+        if (rc != DOS_OK) {
+          err.store(rc);
+          return;
+        }
+        mine[slot] = -1;
       }
-      bar.arrive_and_wait();
-      if (tid == 0 && err.load(std::memory_order_relaxed) == DOS_OK) {
-        const int rc = ring.ship(ring.ctx, c, slot, c0, len);
-        if (rc != DOS_OK) err.store(rc);
+      uint16_t* w = base + (int64_t)slot * ring.chunk;
+      t.adam_cached(p + c0, m + c0, v + c0, static_cast<const char*>(g) + gsz * c0, gt, w, lt, 0, len, s);
+      const int64_t id = ring.post(ring.ctx, w, c0, len);
+      if (id < 0) {
+        err.store((int)id);
+        return;
       }
+      mine[slot] = id;
+      slot = (slot + 1) % ring.nslots;
     }
   });
   return err.load();

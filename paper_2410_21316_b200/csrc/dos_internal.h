@@ -59,34 +59,37 @@ struct dos_hk_table {
   void (*adam_cached)(float*, float*, float*, const void*, int, void*, int, int64_t, int64_t, const dos_kscal&);
 };
 
-// H1 through a staging ring (the working copy of host-updated subgroups):
-// the subgroup is processed in chunks of `chunk` elements by the whole team;
-// chunk c's working copy goes (regular stores) into ring slot
-// (first + c) % nslots, and after the team's barrier thread 0 calls
-// ship(ctx, c, slot, offset, count) — the engine enqueues the slot's H2D copy —
-// while the other threads
-// already work on chunk c + 1.  Before chunk c + 1's barrier, thread 0 calls
-// reclaim(ctx, slot) for the slot chunk c + 1 writes (waits until its
-// previous copy has left the host).  Small slots stay in the LLC, so the
-// working copy never makes a host-DRAM round trip.
+// H1 through per-thread staging rings (the working copy of host-updated
+// subgroups): every team thread updates its contiguous slice of the subgroup
+// in chunks of `chunk` elements; a chunk's working copy goes (regular
+// stores) into one of the thread's own `nslots` slots, and the thread hands
+// it to the shuttle with post() and moves on — no barrier, no CUDA call.  A
+// slot is reused only after wait() shows its previous chunk was served.  The
+// slots (nslots * chunk * 2 B per thread) stay in the core's L2 / the LLC,
+// so the working copy never makes a host-DRAM round trip.
 struct dos_ring {
-  uint16_t* slots;  // nslots * chunk elements, pinned
+  uint16_t* slots;  // nthreads * nslots * chunk elements, pinned and device-mapped
+  int nthreads;     // threads the slots are laid out for (>= the team's)
   int nslots;
   int64_t chunk;
-  int64_t first;    // chunk 0 goes to slot first % nslots (the ring runs on across subgroups)
   void* ctx;
-  int (*ship)(void* ctx, int64_t chunk_index, int slot, int64_t offset, int64_t count);
-  int (*reclaim)(void* ctx, int slot);
+  // post: the copy of `count` elements of `slot` to element `offset` of the
+  // subgroup's device working copy; returns the shuttle descriptor (>= 0) or
+  // a negative DOS_E* code.  wait: block until that descriptor was served.
+  int64_t (*post)(void* ctx, const uint16_t* slot, int64_t offset, int64_t count);
+  int (*wait)(void* ctx, int64_t id);
 };
+// `last` (nthreads * nslots entries, -1 = idle) receives each slot's last
+// descriptor: the caller waits for them before the subgroup counts as shipped.
 int dos_host_adam_ring(float* p, float* m, float* v, const void* g, int gt, int lt, int64_t n, const dos_kscal& s,
-                       int nthreads, const dos_ring& ring);
+                       int nthreads, const dos_ring& ring, int64_t* last);
 extern const dos_hk_table dos_hk_avx512;
 extern const dos_hk_table dos_hk_avx2;
 extern const dos_hk_table dos_hk_generic;
 
 // The shuttle (dos_cuda.cu): a persistent kernel serving copy descriptors
 // posted by the host lane into mapped pinned memory (see k_shuttle).
-#define DOS_SHUTTLE_Q 256
+#define DOS_SHUTTLE_Q 1024
 struct dos_shuttle_desc {  // 32 B; `id` (= descriptor number + 1) is written last
   uint64_t src, dst;       // device-accessible addresses (host memory: its device alias)
   uint32_t bytes;
@@ -100,7 +103,6 @@ struct dos_shuttle_ctl {
   uint32_t done[DOS_SHUTTLE_Q];  // kernel: descriptor number + 1 of the last completed one per queue slot
   dos_shuttle_desc q[DOS_SHUTTLE_Q];
 };
-int dos_shuttle_launch(dos_shuttle_ctl* ctl_dev, uint32_t* flags_dev, uint32_t* cnt_dev, uint32_t first, int nctas,
-                       cudaStream_t st);
+int dos_shuttle_launch(dos_shuttle_ctl* ctl_dev, uint32_t* flags_dev, uint32_t first, int nctas, cudaStream_t st);
 // SMs kept free of K1's persistent grid while a shuttle runs.
 void dos_reserve_sms(int n);

@@ -46,3 +46,25 @@ def test_b200_arm_contract():
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["phase_roofline"]["frac"] > 0 and d["copy_streams"]["frac"] > 0
+
+
+def test_joint_bound_is_a_lower_bound_for_every_split():
+    """phase_roofline.joint_bound: min over the streamed fraction of the
+    slowest resource — never above the bound of any concrete split, and the
+    binding resources balance at the optimum."""
+    import sys
+
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    D, S = 5.6e9, 1.4e9
+    hbm, link, dram, h1 = 6.5e12, 48e9, 180e9, 5e9
+    for flush in (False, True):
+        jb = bench.joint_bound(D, S, hbm, link, dram, h1, flush)
+        gB = 2.0 if flush else 0.0
+        for x in (0.0, 0.1, 0.25, 0.5, 0.75, 1.0):
+            t = max(28 * (S + x * D) / hbm, max((12 * x + 2 * (1 - x)) * D, (12 * x + gB * (1 - x)) * D) / link,
+                    (24 * x + (30 + gB) * (1 - x)) * D / dram, (1 - x) * D / h1)
+            assert jb["ideal_ms"] <= t * 1e3 + 1e-6
+        at = jb["bounds_ms_at_optimum"]
+        assert abs(at["link"] - at["host_dram"]) / jb["ideal_ms"] < 0.01  # link and DRAM balance here

@@ -1,6 +1,7 @@
 """The host lane's working-copy staging ring (dos_host_adam_ring + the
 shuttle kernel): host-updated subgroups' working copy goes H2D in
-LLC-resident chunks during the CPU update instead of through the host image.
+chunks from every team thread's own L2/LLC-resident slots during the CPU
+update, instead of through the host image.
 Bit-exact against the oracle with many chunks per subgroup, ragged chunks,
 two-slot wrap-around across subgroups, every plan shape, and with the ring
 off (the A/B baseline).  The ring configuration is read once per process, so
@@ -47,8 +48,9 @@ print("ring ok")
 
 @pytest.mark.parametrize("env", [
     {},  # default ring (4 x 512K: one chunk per small subgroup)
-    {"DOS_W_RING_CHUNK": "4096", "DOS_W_RING_SLOTS": "2"},  # many ragged chunks, tight wrap-around
-    {"DOS_W_RING_CHUNK": "12288", "DOS_W_RING_SLOTS": "3", "DOS_SHUTTLE_CTAS": "1"},
+    {"DOS_W_RING_CHUNK": "4096", "DOS_W_RING_SLOTS": "2"},  # many ragged chunks per thread, tight reuse
+    {"DOS_W_RING_CHUNK": "1024", "DOS_W_RING_SLOTS": "1", "DOS_SHUTTLE_CTAS": "1"},  # one slot, one CTA
+    {"DOS_W_RING_CHUNK": "12288", "DOS_W_RING_SLOTS": "3", "DOS_SHUTTLE_CTAS": "3"},
     # every stream on ONE hardware queue: a wait at the head of any stream blocks
     # all the others queued behind it.  The engine must still finish: every
     # GPU-side wait is on a host action emitted earlier, and the ring's copies
