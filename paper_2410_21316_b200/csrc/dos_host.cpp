@@ -12,6 +12,7 @@
 #include <sched.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 #include <sys/mman.h>
 #include <sys/syscall.h>
@@ -199,10 +200,22 @@ extern "C" int dos_set_host_threads(int n) {
 }
 
 // ---------------------------------------------------------------- H1
+// How H1 stores the working copy into a host image: non-temporal 64-byte
+// stores (default: no read-for-ownership) or regular cached stores
+// (DOS_H1_WSTORE=cached; an A/B knob, profiles/r02_ring_ab.json).
+static bool h1_cached_w() {
+  static const bool c = [] {
+    const char* e = getenv("DOS_H1_WSTORE");
+    return e && strcmp(e, "cached") == 0;
+  }();
+  return c;
+}
+
 int dos_host_adam(float* p, float* m, float* v, const void* g, int gt, void* lp, int lt, int64_t n,
                   const dos_kscal& s, int nthreads) {
   const dos_hk_table& t = hk();
-  parallel_chunks(n, nthreads, [&](int64_t lo, int64_t hi) { t.adam(p, m, v, g, gt, lp, lt, lo, hi, s); });
+  const auto fn = h1_cached_w() ? t.adam_cached : t.adam;
+  parallel_chunks(n, nthreads, [&](int64_t lo, int64_t hi) { fn(p, m, v, g, gt, lp, lt, lo, hi, s); });
   return DOS_OK;
 }
 
