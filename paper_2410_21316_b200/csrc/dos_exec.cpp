@@ -48,10 +48,17 @@ namespace {
 typedef CUresult (*pfn_wait_value32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 typedef CUresult (*pfn_write_value32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 
-// Working-copy staging ring of the host lane (dos_host_adam_ring): slots x
-// chunk elements of pinned memory, small enough to stay in the host's LLC.
-// DOS_W_RING=0 turns it off (H1 then writes the working copy into the host
-// image with non-temporal stores and H2D_PARAMS16 ships it from there).
+// Working-copy staging rings of the host lane (dos_host_adam_ring + the
+// shuttle kernel): per team thread `slots` x `chunk` elements of pinned
+// memory, meant to stay in the host's caches so the working copy of a
+// host-updated subgroup never makes a DRAM round trip.  OFF by default
+// (DOS_W_RING=1 turns it on): measured on the 16-core B200 host it is slower
+// than H1 storing the working copy non-temporally into the host image and
+// H2D_PARAMS16 shipping it (1035-1122 ms vs 976-997 ms for the 7B phase,
+// profiles/r02_ring_ab.jsonl) — the slots' regular stores pay a
+// read-for-ownership after every device read, as cached stores into the
+// image do (1092-1126 ms), and the zero-copy pull shares the link with the
+// copy engines (profiles/r02_zero_copy_pull.json).
 struct RingCfg {
   bool on;
   int slots;      // per team thread
@@ -60,7 +67,7 @@ struct RingCfg {
 };
 const RingCfg& ring_cfg() {
   static RingCfg c = [] {
-    RingCfg r{true, 4, 1 << 16, 8};  // per thread 4 x 64K elements (512 KB of bf16: the core's L2)
+    RingCfg r{false, 4, 1 << 16, 16};  // per thread 4 x 64K elements (512 KB of bf16: the core's L2)
     if (const char* e = getenv("DOS_W_RING")) r.on = strcmp(e, "0") != 0;
     if (const char* e = getenv("DOS_W_RING_SLOTS")) r.slots = std::max(1, std::min(64, atoi(e)));
     if (const char* e = getenv("DOS_W_RING_CHUNK")) r.chunk = std::max<int64_t>(1024, atoll(e)) & ~int64_t(63);

@@ -1,5 +1,6 @@
 """The host lane's working-copy staging ring (dos_host_adam_ring + the
-shuttle kernel): host-updated subgroups' working copy goes H2D in
+shuttle kernel; opt-in, DOS_W_RING=1 — slower than the default on the
+measured host, kept as an A/B arm): host-updated subgroups' working copy goes H2D in
 chunks from every team thread's own L2/LLC-resident slots during the CPU
 update, instead of through the host image.
 Bit-exact against the oracle with many chunks per subgroup, ragged chunks,
@@ -47,17 +48,18 @@ print("ring ok")
 
 
 @pytest.mark.parametrize("env", [
-    {},  # default ring (4 x 512K: one chunk per small subgroup)
-    {"DOS_W_RING_CHUNK": "4096", "DOS_W_RING_SLOTS": "2"},  # many ragged chunks per thread, tight reuse
-    {"DOS_W_RING_CHUNK": "1024", "DOS_W_RING_SLOTS": "1", "DOS_SHUTTLE_CTAS": "1"},  # one slot, one CTA
-    {"DOS_W_RING_CHUNK": "12288", "DOS_W_RING_SLOTS": "3", "DOS_SHUTTLE_CTAS": "3"},
+    {"DOS_W_RING": "1"},  # ring on (off by default): 4 x 64K per thread, 16 shuttle CTAs
+    {"DOS_W_RING": "1", "DOS_W_RING_CHUNK": "4096", "DOS_W_RING_SLOTS": "2"},  # many ragged chunks, tight reuse
+    {"DOS_W_RING": "1", "DOS_W_RING_CHUNK": "1024", "DOS_W_RING_SLOTS": "1", "DOS_SHUTTLE_CTAS": "1"},
+    {"DOS_W_RING": "1", "DOS_W_RING_CHUNK": "12288", "DOS_W_RING_SLOTS": "3", "DOS_SHUTTLE_CTAS": "3"},
     # every stream on ONE hardware queue: a wait at the head of any stream blocks
     # all the others queued behind it.  The engine must still finish: every
     # GPU-side wait is on a host action emitted earlier, and the ring's copies
     # are served by a kernel launched before anything else of the phase
-    {"CUDA_DEVICE_MAX_CONNECTIONS": "1", "DOS_W_RING_CHUNK": "12288", "DOS_W_RING_SLOTS": "3"},
-    {"CUDA_DEVICE_MAX_CONNECTIONS": "1", "DOS_W_RING": "0"},
-    {"DOS_W_RING": "0"},  # off: H1 -> host image -> H2D_PARAMS16
+    {"CUDA_DEVICE_MAX_CONNECTIONS": "1", "DOS_W_RING": "1", "DOS_W_RING_CHUNK": "12288", "DOS_W_RING_SLOTS": "3"},
+    {"CUDA_DEVICE_MAX_CONNECTIONS": "1"},  # the default path (ring off) on one hardware queue
+    {"DOS_H1_WSTORE": "cached"},  # H1's cached-store variant (A/B knob)
+    {},  # default: H1 -> host image (NT stores) -> H2D_PARAMS16
 ])
 def test_ring_bit_exact(env):
     proc = subprocess.run([sys.executable, "-c", CHECK], cwd=ROOT, env=dict(os.environ, **env), capture_output=True,
