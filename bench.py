@@ -1040,7 +1040,8 @@ class B200Bench:
                 # this residency against the pure offload-to-CPU schedule (which keeps
                 # no state in HBM): what capacity-aware residency buys, stated as such
                 v["speedup_vs_offload_to_cpu_at_0pct"] = offload_ms / ms
-            if sweep and ratio == 0.0:
+            if sweep and not any("stride_sweep_ms" in u for u in entry["variants"]):
+                # (at 0% residency when the host holds it, else on the capacity-aware split)
                 # the GPU-subgroup-fraction sweep (configs[4]): every stride + ALL_CPU, one timed step each
                 sw = {}
                 for k in (1, 2, 3, 4, 5, 6):

@@ -15,9 +15,9 @@ def launches(path):
         if r["Metric Name"] != "gpu__time_duration.sum":
             continue
         name = r["Kernel Name"]
-        if "k_adam" in name or "k_down" in name or "k_up" in name:
-            import re
+        import re
 
+        if re.search(r"(^|::|\s)k_(adam|down|up|reduce|coherence|shuttle)", name):
             mt = re.search(r"(k_[a-z_]+)(<[^>]*>)?", name)
             short = "libdos:" + (mt.group(1) + (mt.group(2) or "") if mt else name[:60])
         else:
