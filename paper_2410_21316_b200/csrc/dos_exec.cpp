@@ -65,6 +65,25 @@ struct RingCfg {
   int64_t chunk;  // elements per slot
   int ctas;       // shuttle CTAs
 };
+// Grad ring of the in-phase flush (dos_gring): `slots` rows of `chunk`
+// elements per team thread.  DOS_G_RING=0 turns it off (whole-subgroup D2H
+// into the host image instead).
+struct GRingCfg {
+  bool on;
+  int slots;
+  int64_t chunk;
+};
+const GRingCfg& gring_cfg() {
+  static GRingCfg c = [] {
+    GRingCfg r{true, 3, 1 << 16};  // 3 rows x 16 threads x 64K elements = 6 MB of bf16
+    if (const char* e = getenv("DOS_G_RING")) r.on = strcmp(e, "0") != 0;
+    if (const char* e = getenv("DOS_G_RING_SLOTS")) r.slots = std::max(1, std::min(64, atoi(e)));
+    if (const char* e = getenv("DOS_G_RING_CHUNK")) r.chunk = std::max<int64_t>(1024, atoll(e)) & ~int64_t(63);
+    return r;
+  }();
+  return c;
+}
+
 const RingCfg& ring_cfg() {
   static RingCfg c = [] {
     RingCfg r{false, 4, 1 << 16, 16};  // per thread 4 x 64K elements (512 KB of bf16: the core's L2)
@@ -94,6 +113,8 @@ struct Job {
   int32_t id, kind, sg;
   std::vector<int32_t> deps, batch;
   cudaEvent_t flushed = nullptr;  // in-phase grad flush of this subgroup (flush_grads)
+  bool gring = false;             // grads arrive row by row through the grad ring
+  uint32_t gseq0 = 0;             // its first row's sequence number
 };
 
 struct Engine {
@@ -114,6 +135,15 @@ struct Engine {
   CUdeviceptr ring_flags_dev = 0;
   int32_t ring_flags_cap = 0;
   pfn_write_value32 write_fn = nullptr;
+  // grad ring (GRingCfg): pinned rows + mapped ready/consumed flags
+  bool gring_phase = false;
+  int gring_k = 0;                  // slice layout's thread count
+  uint16_t* gring_mem = nullptr;
+  size_t gring_bytes = 0;
+  uint32_t* gring_flags = nullptr;  // [0, slots): ready; [slots, 2 slots): consumed
+  CUdeviceptr gring_flags_dev = 0;
+  std::vector<int> gring_counts;
+  uint32_t gring_seq = 0;           // rows issued so far (monotonic across phases)
   // the shuttle: descriptor queue in mapped pinned memory
   dos_shuttle_ctl* sh_ctl = nullptr;
   dos_shuttle_ctl* sh_ctl_dev = nullptr;
@@ -306,6 +336,16 @@ struct Engine {
       if (code != DOS_OK) msg = dos_last_error();
       return code;
     }
+    if (j.kind == DOS_CPU_UPDATE && j.gring) {
+      const int64_t a = sg_start[j.sg], n = sg_size[j.sg];
+      const GRingCfg& gc = gring_cfg();
+      dos_gring r{gring_mem, gc.slots, gc.chunk, gring_k, gring_flags, gring_flags + gc.slots, gring_counts.data(),
+                  j.gseq0};
+      void* lp = fuse ? static_cast<void*>(static_cast<char*>(S.host_lowp) + 2 * a) : nullptr;
+      const int rc = dos_host_adam_gring(S.host_p + a, S.host_m + a, S.host_v + a, lt, lp, lt, n, K, r);
+      if (rc != DOS_OK) msg = dos_last_error();
+      return rc;
+    }
     if (j.kind == DOS_CPU_UPDATE) {
       const int64_t a = sg_start[j.sg], n = sg_size[j.sg];
       const void* g = static_cast<const char*>(S.host_g) + 2 * a;
@@ -378,7 +418,20 @@ struct Engine {
       j.batch.assign(a->batch, a->batch + a->batch_len);
       for (int32_t b : j.batch)
         if (b < 0 || b >= S.num_subgroups) return fail(DOS_EINVAL, "downscale batch names a bad subgroup");
-      if (S.flush_grads && a->kind == DOS_CPU_UPDATE) {
+      if (S.flush_grads && a->kind == DOS_CPU_UPDATE && gring_phase) {
+        // the grads of this subgroup D2H row by row through the grad ring,
+        // every copy enqueued now (FIFO-safe: each waits only for rows the
+        // host consumes before it needs this subgroup)
+        const int64_t start = sg_start[sg], n = sg_size[sg];
+        if (gsrc.n > 0) {  // fused reduce-scatter of this subgroup, in place in dev_g, ahead of its rows
+          const int rc = dos_reduce_launch(static_cast<char*>(const_cast<void*>(S.dev_g)) + 2 * start, S.lowp_dtype, n,
+                                           dos_gsrc_offset(gsrc, start), gst);
+          if (rc != DOS_OK) return fail(rc, dos_last_error());
+        }
+        const int rc = enqueue_grad_rows(start, n, &j.gseq0);
+        if (rc != DOS_OK) return fail(rc, dos_last_error());
+        j.gring = true;
+      } else if (S.flush_grads && a->kind == DOS_CPU_UPDATE) {
         // §8(f) row 1 inside the phase: this subgroup's half-precision grads
         // D2H on their own stream, in emission (= subgroup) order
         const int64_t start = sg_start[sg], n = sg_size[sg];
@@ -423,6 +476,45 @@ struct Engine {
     rc = enqueue_gpu(a, s);
     if (rc != DOS_OK) return fail(rc, dos_last_error());
     DOS_CU(cudaEventRecord(ev_e[a->id], s));
+    return DOS_OK;
+  }
+
+  // The grad ring's D2H rows of one subgroup on the grad stream.
+  int enqueue_grad_rows(int64_t start, int64_t n, uint32_t* seq0) {
+    const GRingCfg& gc = gring_cfg();
+    const int k = gring_k;
+    const int64_t C = gc.chunk, per = dos_gring_per(n, k), rows = n > 0 ? dos_gring_rows(n, k, C) : 0;
+    const uint32_t R = (uint32_t)gc.slots;
+    *seq0 = gring_seq;
+    const char* dev_g = static_cast<const char*>(S.dev_g) + 2 * start;
+    for (int64_t c = 0; c < rows; ++c) {
+      const uint32_t seq = gring_seq++;
+      const uint32_t slot = seq % R;
+      char* dst = reinterpret_cast<char*>(gring_mem) + (size_t)slot * k * C * 2;
+      if (seq >= R &&  // the slot's previous row must have been consumed by every thread
+          wait_fn((CUstream)gst, gring_flags_dev + 4 * (CUdeviceptr)(R + slot), seq - R + 1, CU_STREAM_WAIT_VALUE_GEQ) !=
+              CUDA_SUCCESS)
+        return dos_set_error(DOS_ECUDA, "cuStreamWaitValue32 (grad ring) failed");
+      bool full = true;
+      for (int t = 0; t < k && full; ++t) {
+        const int64_t lo = std::min(n, per * t), hi = std::min(n, lo + per);
+        if (lo + c * C < hi && lo + (c + 1) * C > hi) full = false;
+        if (lo + c * C >= hi) full = false;
+      }
+      if (full) {
+        DOS_CU(cudaMemcpy2DAsync(dst, (size_t)C * 2, dev_g + 2 * c * C, (size_t)per * 2, (size_t)C * 2, (size_t)k,
+                                 cudaMemcpyDeviceToHost, gst));
+      } else {
+        for (int t = 0; t < k; ++t) {
+          const int64_t lo = std::min(n, per * t), hi = std::min(n, lo + per), c0 = lo + c * C;
+          if (c0 >= hi) continue;
+          DOS_CU(cudaMemcpyAsync(dst + (size_t)t * C * 2, dev_g + 2 * c0, (size_t)std::min(C, hi - c0) * 2,
+                                 cudaMemcpyDeviceToHost, gst));
+        }
+      }
+      if (write_fn((CUstream)gst, gring_flags_dev + 4 * (CUdeviceptr)slot, seq + 1, 0) != CUDA_SUCCESS)
+        return dos_set_error(DOS_ECUDA, "cuStreamWriteValue32 (grad ring) failed");
+    }
     return DOS_OK;
   }
 
@@ -662,6 +754,31 @@ struct Engine {
       ring_mem_dev = static_cast<uint16_t*>(dptr);
       ring_last.assign((size_t)ring_threads * rc.slots, -1);
     }
+    // the grad ring: in-phase flush of 16-bit grads, the host lane's slices
+    // laid out for the team it will run on
+    gring_phase = gring_cfg().on && S.flush_grads && !S.host_io && S.host_updates != 0 && wait_fn && write_fn &&
+                  wait_value_ok && !ring_phase;
+    if (gring_phase) {
+      const GRingCfg& gc = gring_cfg();
+      const int team = dos_host_threads();
+      gring_k = host_threads > 0 ? std::min(host_threads, team) : team;
+      const size_t bytes = (size_t)gc.slots * gring_k * gc.chunk * 2;
+      if (bytes > gring_bytes) {
+        if (gring_mem) cudaFreeHost(gring_mem);
+        gring_mem = nullptr;
+        DOS_CU(cudaHostAlloc(reinterpret_cast<void**>(&gring_mem), bytes, cudaHostAllocDefault));
+        gring_bytes = bytes;
+      }
+      if (!gring_flags) {
+        DOS_CU(cudaHostAlloc(reinterpret_cast<void**>(&gring_flags), 2 * 64 * 4, cudaHostAllocMapped));
+        memset(gring_flags, 0, 2 * 64 * 4);
+        void* dptr = nullptr;
+        DOS_CU(cudaHostGetDevicePointer(&dptr, gring_flags, 0));
+        gring_flags_dev = (CUdeviceptr)dptr;
+        gring_seq = 0;
+      }
+      gring_counts.assign(gc.slots, 0);
+    }
     if (ring_phase && !sh_ctl) {
       DOS_CU(cudaHostAlloc(reinterpret_cast<void**>(&sh_ctl), sizeof(dos_shuttle_ctl), cudaHostAllocMapped));
       memset(sh_ctl, 0, sizeof(dos_shuttle_ctl));
@@ -822,6 +939,8 @@ struct Engine {
     if (ring_flags) cudaFreeHost(ring_flags);
     if (ring_mem) cudaFreeHost(ring_mem);
     if (sh_ctl) cudaFreeHost(sh_ctl);
+    if (gring_mem) cudaFreeHost(gring_mem);
+    if (gring_flags) cudaFreeHost(gring_flags);
   }
 };
 

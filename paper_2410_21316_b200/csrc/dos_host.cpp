@@ -262,6 +262,40 @@ int dos_host_adam_ring(float* p, float* m, float* v, const void* g, int gt, int 
   return err.load();
 }
 
+int dos_host_adam_gring(float* p, float* m, float* v, int gt, void* lp, int lt, int64_t n, const dos_kscal& s,
+                        const dos_gring& r) {
+  if (n == 0) return DOS_OK;
+  if (gt == DOS_F32 || r.nslots < 1 || r.chunk < 64 || !r.slots || !r.ready || !r.consumed || !r.counts)
+    return dos_set_error(DOS_EINVAL, "grad ring: bad configuration");
+  const dos_hk_table& t = hk();
+  const std::shared_ptr<Team> hold = team();
+  Team& tm = *hold;
+  const int k = r.nthreads;
+  if (k > tm.size()) return dos_set_error(DOS_EINVAL, "grad ring laid out for %d threads, team has %d", k, tm.size());
+  const int64_t per = dos_gring_per(n, k), row = (int64_t)k * r.chunk;
+  tm.run(k, [&](int tid) {
+    const int64_t lo = std::min<int64_t>(n, per * tid), hi = std::min<int64_t>(n, lo + per);
+    for (int64_t c = 0; lo + c * r.chunk < hi; ++c) {
+      const uint32_t seq = r.seq0 + (uint32_t)c;
+      const int slot = (int)(seq % (uint32_t)r.nslots);
+      for (int i = 0; (int32_t)(__atomic_load_n(&r.ready[slot], __ATOMIC_ACQUIRE) - (seq + 1)) < 0; ++i) {
+        if (i < 1024) __builtin_ia32_pause();
+        else std::this_thread::yield();
+      }
+      const int64_t c0 = lo + c * r.chunk, len = std::min(r.chunk, hi - c0);
+      const uint16_t* g = r.slots + (int64_t)slot * row + (int64_t)tid * r.chunk;
+      t.adam(p + c0, m + c0, v + c0, g, gt, lp ? static_cast<char*>(lp) + 2 * c0 : nullptr, lp ? lt : DOS_NONE, 0,
+             len, s);
+      // the last thread done with this row hands its slot back to the copy engine
+      if (__atomic_add_fetch(&r.counts[slot], 1, __ATOMIC_ACQ_REL) == dos_gring_row_threads(n, k, r.chunk, c)) {
+        __atomic_store_n(&r.counts[slot], 0, __ATOMIC_RELAXED);
+        __atomic_store_n(&r.consumed[slot], seq + 1, __ATOMIC_RELEASE);
+      }
+    }
+  });
+  return DOS_OK;
+}
+
 int dos_host_down(const float* x, void* out, int ot, int64_t n, int nthreads) {
   const dos_hk_table& t = hk();
   parallel_chunks(n, nthreads, [&](int64_t lo, int64_t hi) { t.down(x, out, ot, lo, hi); });

@@ -106,3 +106,42 @@ struct dos_shuttle_ctl {
 int dos_shuttle_launch(dos_shuttle_ctl* ctl_dev, uint32_t* flags_dev, uint32_t first, int nctas, cudaStream_t st);
 // SMs kept free of K1's persistent grid while a shuttle runs.
 void dos_reserve_sms(int n);
+
+// In-phase grad flush through a cache-sized ring (flush_grads): the engine
+// pre-enqueues, at CPU_UPDATE submit, the D2H copies of a subgroup's grads
+// row by row into `nslots` pinned slots (row = the next `chunk` elements of
+// every team thread's slice), each copy gated on the slot's previous row
+// having been consumed and followed by a ready flag; the team threads spin on
+// the ready flags and read the grads from the slots, which the copy engine
+// just wrote (with the host's DMA write-allocate into the LLC they never make
+// a DRAM round trip).  Every wait is enqueued at submit time for host work
+// emitted earlier, so it stays deadlock-free when streams share a hardware
+// queue.
+struct dos_gring {
+  const uint16_t* slots;   // nslots rows of nthreads * chunk elements
+  int nslots;
+  int64_t chunk;           // elements per thread per row
+  int nthreads;            // the slice layout's thread count
+  const uint32_t* ready;   // mapped, per slot: seq + 1 once the row landed
+  uint32_t* consumed;      // mapped, per slot: seq + 1 once every thread used the row
+  int* counts;             // per slot: threads done with the current row
+  uint32_t seq0;           // sequence number of the subgroup's row 0
+};
+inline int64_t dos_gring_per(int64_t n, int k) { return ((n + k - 1) / k + 63) & ~int64_t(63); }
+// rows of a subgroup of n elements (thread 0's slice is the longest)
+inline int64_t dos_gring_rows(int64_t n, int k, int64_t chunk) {
+  const int64_t per = dos_gring_per(n, k), l0 = per < n ? per : n;
+  return (l0 + chunk - 1) / chunk;
+}
+// threads whose slice has a row c
+inline int dos_gring_row_threads(int64_t n, int k, int64_t chunk, int64_t c) {
+  const int64_t per = dos_gring_per(n, k);
+  int cnt = 0;
+  for (int t = 0; t < k; ++t) {
+    const int64_t lo = per * t < n ? per * t : n, hi = lo + per < n ? lo + per : n;
+    if (lo + c * chunk < hi) ++cnt;
+  }
+  return cnt;
+}
+int dos_host_adam_gring(float* p, float* m, float* v, int gt, void* lp, int lt, int64_t n, const dos_kscal& s,
+                        const dos_gring& r);

@@ -123,6 +123,9 @@ class DeviceResidency:
         if name == "_w":
             self._d2h_lowp(opt._w, self.model16)
             return
+        if name == "_g":
+            self._d2h_lowp(opt._g, self.grads)
+            return
         k = ("_p", "_m", "_v").index(name)
         dst = getattr(opt, name)
         opt.ensure_host(self.static_set, "state")
@@ -151,7 +154,7 @@ class DeviceResidency:
         n = len(self.opt.subgroups)
         self.opt.ensure_host(range(n), "state")
         self.opt.ensure_host(range(n), "lowp")
-        for name in ("_w", "_p", "_m", "_v"):
+        for name in ("_w", "_g", "_p", "_m", "_v"):
             self.sync_host(name)
 
     def host_modified(self) -> None:
@@ -269,9 +272,11 @@ class DeviceResidency:
                     self._static_ptrs[3 * sg + k] = self.static_sg[sg][k].data_ptr()
         self.static_set = static_set
 
-    def after_phase(self, host_io: bool = False) -> None:
+    def after_phase(self, host_io: bool = False, flush_grads: bool = False) -> None:
         if not host_io:  # with host_io the engine mirrored the working copy to the host
             self.host_stale.add("_w")
+        if flush_grads:  # the device grads are the step's (reduced) grads; the host image may
+            self.host_stale.add("_g")  # not hold them (the grad ring bypasses it)
         if self.static_set:
             self.host_stale.update(("_p", "_m", "_v"))
 

@@ -240,7 +240,7 @@ def execute_plan(
         target.finish(raise_errors=False)
         raise
     measured_events = target.finish()
-    target.residency.after_phase(host_io)
+    target.residency.after_phase(host_io, flush_grads)
     measured = build_timeline(plan, measured_events, sizes) if measured_events else None
     if validate_measured and measured_events and not _under_profiler():
         validate_schedule(plan, measured_events, target, check_streams=False, max_windows=target.num_slots,

@@ -368,9 +368,7 @@ class ShardedOptimizer:
 
     @property
     def grads16(self) -> np.ndarray:
-        if self._sparse is not None:
-            self.ensure_host(range(len(self.subgroups)), "lowp")
-        return self._g
+        return self._host("_g")  # after an in-phase grad flush the device holds the step's grads
 
     @property
     def total_params(self) -> int:
