@@ -66,8 +66,13 @@ struct RingCfg {
   int ctas;       // shuttle CTAs
 };
 // Grad ring of the in-phase flush (dos_gring): `slots` rows of `chunk`
-// elements per team thread.  DOS_G_RING=0 turns it off (whole-subgroup D2H
-// into the host image instead).
+// elements per team thread.  OFF by default (DOS_G_RING=1 turns it on):
+// measured on the 16-core B200 host it is slower than the whole-subgroup D2H
+// into the host image (7B phase 1167-1354 ms vs 974-1022 ms,
+// profiles/r02_gring_ab.jsonl): the row copies share the copy engines with
+// the streamed windows' 400 MB flushes, so a row the team waits for can sit
+// behind one for milliseconds, and a ring small enough to stay in the LLC
+// has well under a millisecond of slack.
 struct GRingCfg {
   bool on;
   int slots;
@@ -75,7 +80,7 @@ struct GRingCfg {
 };
 const GRingCfg& gring_cfg() {
   static GRingCfg c = [] {
-    GRingCfg r{true, 3, 1 << 16};  // 3 rows x 16 threads x 64K elements = 6 MB of bf16
+    GRingCfg r{false, 3, 1 << 16};  // 3 rows x 16 threads x 64K elements = 6 MB of bf16
     if (const char* e = getenv("DOS_G_RING")) r.on = strcmp(e, "0") != 0;
     if (const char* e = getenv("DOS_G_RING_SLOTS")) r.slots = std::max(1, std::min(64, atoi(e)));
     if (const char* e = getenv("DOS_G_RING_CHUNK")) r.chunk = std::max<int64_t>(1024, atoll(e)) & ~int64_t(63);

@@ -59,10 +59,11 @@ print("ring ok")
     {"CUDA_DEVICE_MAX_CONNECTIONS": "1", "DOS_W_RING": "1", "DOS_W_RING_CHUNK": "12288", "DOS_W_RING_SLOTS": "3"},
     {"CUDA_DEVICE_MAX_CONNECTIONS": "1"},  # the default path (ring off) on one hardware queue
     {"DOS_H1_WSTORE": "cached"},  # H1's cached-store variant (A/B knob)
-    # the in-phase grad flush's ring (on by default): tiny rows, one slot
-    {"DOS_G_RING_CHUNK": "1024", "DOS_G_RING_SLOTS": "1"},
-    {"DOS_G_RING_CHUNK": "4096", "DOS_G_RING_SLOTS": "2", "CUDA_DEVICE_MAX_CONNECTIONS": "1"},
-    {"DOS_G_RING": "0"},  # whole-subgroup D2H into the host image
+    # the in-phase grad flush's ring (opt-in A/B arm): default rows, tiny rows
+    # with one slot, and on one hardware queue
+    {"DOS_G_RING": "1"},
+    {"DOS_G_RING": "1", "DOS_G_RING_CHUNK": "1024", "DOS_G_RING_SLOTS": "1"},
+    {"DOS_G_RING": "1", "DOS_G_RING_CHUNK": "4096", "DOS_G_RING_SLOTS": "2", "CUDA_DEVICE_MAX_CONNECTIONS": "1"},
     {},  # default: H1 -> host image (NT stores) -> H2D_PARAMS16
 ])
 def test_ring_bit_exact(env):
