@@ -26,8 +26,12 @@ def _bits(t) -> np.ndarray:
     return t.detach().view(torch.int32 if t.element_size() == 4 else torch.int16).cpu().numpy().copy()
 
 
-@pytest.mark.parametrize("params, ratio, stride", [(7e9, 0.2, 5), (13e9, "auto", 6), (8.75e9, 0.5, 3)])
-def test_full_size_sampled_parity(params, ratio, stride):
+@pytest.mark.parametrize("params, ratio, stride, flush", [(7e9, 0.2, 5, True), (13e9, "auto", 6, False),
+                                                          (8.75e9, 0.5, 3, True)])
+def test_full_size_sampled_parity(params, ratio, stride, flush):
+    """flush: the bench's mode — the host-updated subgroups' grads flushed D2H
+    inside the phase, and the checked step asserts coherence over every
+    element of every subgroup ("full")."""
     from bench import fill_shard, host_available_bytes
     from oracle import c_oracle
 
@@ -65,7 +69,8 @@ def test_full_size_sampled_parity(params, ratio, stride):
 
     snap = {i: (home(i), _bits(res.grads[opt.subgroups[i].slice])) for i in sample}
     step = opt.step + 1
-    D.execute_plan(opt, plan, prof, hyper)  # step 2 (the checked one)
+    D.execute_plan(opt, plan, prof, hyper, flush_grads=flush,
+                   check_coherence="full" if flush else "sampled")  # step 2 (the checked one)
     torch.cuda.synchronize()
     for i in sorted(sample):
         (p, m, v), g = snap[i]
