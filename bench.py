@@ -1029,8 +1029,12 @@ class B200Bench:
             rplan = self.policy._quiet_plan(nsg, D.ALL_CPU, ratio, self.placement)
             self.phase(rplan, opt=opt)
             ref_ms = self.timed(lambda: self.phase(rplan, opt=opt), steps)
-            v.update({"stride": plan.stride, "ms_per_step": ms, "value": total / (ms * 1e-3),
-                      "all_cpu_ms_per_step": ref_ms, "all_cpu_value": total / (ref_ms * 1e-3),
+            # rank slices: one rank of the config with the whole host to itself,
+            # so only its own params count (a full run's total is not implied)
+            unit_params = P_rank if entry["rank_slices"] else total
+            v.update({"stride": plan.stride, "ms_per_step": ms, "value": unit_params / (ms * 1e-3),
+                      "value_scope": "this rank's params" if entry["rank_slices"] else "all ranks' params",
+                      "all_cpu_ms_per_step": ref_ms, "all_cpu_value": unit_params / (ref_ms * 1e-3),
                       # same HBM budget for both schedules (the residents update on the GPU in both)
                       "speedup_vs_all_cpu": ref_ms / ms,
                       "measured_ms_by_stride": {str(k): t / 1e6 for k, t in sorted(tuner.measured.items())}})
