@@ -211,10 +211,19 @@ static bool h1_cached_w() {
   return c;
 }
 
+// DOS_H1_NT=all: p, m, v written back with streaming stores too (A/B knob).
+static bool h1_nt_all() {
+  static const bool c = [] {
+    const char* e = getenv("DOS_H1_NT");
+    return e && strcmp(e, "all") == 0;
+  }();
+  return c;
+}
+
 int dos_host_adam(float* p, float* m, float* v, const void* g, int gt, void* lp, int lt, int64_t n,
                   const dos_kscal& s, int nthreads) {
   const dos_hk_table& t = hk();
-  const auto fn = h1_cached_w() ? t.adam_cached : t.adam;
+  const auto fn = h1_cached_w() ? t.adam_cached : h1_nt_all() ? t.adam_nta : t.adam;
   parallel_chunks(n, nthreads, [&](int64_t lo, int64_t hi) { fn(p, m, v, g, gt, lp, lt, lo, hi, s); });
   return DOS_OK;
 }

@@ -59,6 +59,7 @@ print("ring ok")
     {"CUDA_DEVICE_MAX_CONNECTIONS": "1", "DOS_W_RING": "1", "DOS_W_RING_CHUNK": "12288", "DOS_W_RING_SLOTS": "3"},
     {"CUDA_DEVICE_MAX_CONNECTIONS": "1"},  # the default path (ring off) on one hardware queue
     {"DOS_H1_WSTORE": "cached"},  # H1's cached-store variant (A/B knob)
+    {"DOS_H1_NT": "all"},  # H1 streaming-stores p, m, v too (A/B knob)
     # the in-phase grad flush's ring (opt-in A/B arm): default rows, tiny rows
     # with one slot, and on one hardware queue
     {"DOS_G_RING": "1"},

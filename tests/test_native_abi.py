@@ -195,3 +195,43 @@ def test_team_resize_while_h1_runs():
         th.join(timeout=120)
     N.check(N.lib().dos_set_host_threads(0))
     assert not th.is_alive() and not errors, errors
+
+
+@pytest.mark.parametrize("knob", ["DOS_H1_NT=all", "DOS_H1_WSTORE=cached"])
+def test_host_store_variants_bit_exact(knob):
+    """The A/B store variants of H1 (streaming p/m/v stores; cached
+    working-copy stores) give the same bits, at aligned and misaligned starts."""
+    import os
+    import subprocess
+    import sys
+
+    code = r"""
+import sys; sys.path.insert(0, ".")
+import numpy as np
+import paper_2410_21316_b200 as D
+from paper_2410_21316_b200 import _native as N
+from oracle import optistate_oracle as O
+rng = np.random.default_rng(3)
+for n, off in ((1 << 20, 0), (300_001, 5), (4097, 17)):
+    p0, m0 = (rng.normal(0, s, n + off).astype(np.float32) for s in (0.02, 1e-3))
+    v0 = (rng.random(n + off) * 1e-4).astype(np.float32)
+    g = O.lowp_from_f32(rng.normal(0, 1, n + off).astype(np.float32), "bf16").view(np.uint16)
+    # page-aligned (pool) buffers, so the 64-byte streaming-store paths run
+    hb = N.HostBuffer((n + off) * 16, register_cuda=False)
+    p, m, v = (hb.array(np.float32, n + off, k * 4 * (n + off)) for k in range(3))
+    w = hb.array(np.uint16, n + off, 12 * (n + off))
+    p[:], m[:], v[:], w[:] = p0, m0, v0, 0
+    sc = N.scalars(1e-3, 0.9, 0.999, 1e-8, np.float32(1 - 0.9 ** 2), np.float32(1 - 0.999 ** 2))
+    N.check(N.lib().dos_adam_step_host(p[off:].ctypes.data, m[off:].ctypes.data, v[off:].ctypes.data,
+                                       g[off:].ctypes.data, N.DOS_BF16, w[off:].ctypes.data, N.DOS_BF16, n, sc, 0))
+    rp, rm, rv = p0[off:].copy(), m0[off:].copy(), v0[off:].copy()
+    O.adam_step(rp, rm, rv, O.f32_from_lowp(g[off:], "bf16"), 1e-3, 0.9, 0.999, 1e-8, 2)
+    assert p[off:].tobytes() == rp.tobytes() and m[off:].tobytes() == rm.tobytes() and v[off:].tobytes() == rv.tobytes()
+    assert w[off:].tobytes() == O.lowp_from_f32(rp, "bf16").view(np.uint16).tobytes()
+print("ok")
+"""
+    k, val = knob.split("=")
+    root = Path(__file__).resolve().parent.parent
+    proc = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, **{k: val}),
+                          capture_output=True, text=True, timeout=300)
+    assert proc.returncode == 0 and "ok" in proc.stdout, proc.stderr[-3000:]
