@@ -22,4 +22,7 @@ O.adam_step(p, m, v, O.f32_from_bf16(gb), 1e-3, 0.9, 0.999, 1e-8, 1)
 assert tp.cpu().numpy().tobytes() == p.tobytes()
 opt = D.ShardedOptimizer.initialize(60_000, 8_200, seed=1, lowp="bf16")
 D.execute_plan(opt, D.build_plan(len(opt.subgroups), 2, 0.2), D.get_profile("h100-node"), D.AdamHyper())
+# the bench's mode: in-phase grad flush (and, with DOS_W_RING / DOS_G_RING, the rings), full coherence check
+D.execute_plan(opt, D.build_plan(len(opt.subgroups), 3, 0.2), D.get_profile("h100-node"), D.AdamHyper(),
+               flush_grads=True, check_coherence="full")
 print("ok")
