@@ -662,6 +662,13 @@ class B200Bench:
         dram_probe = raw.get("host_dram", {})
         dram_Bps = max(dram_probe.get("peak_GBs", 0.0), raw.get("h1_with_dma", {}).get("host_dram_GBs_combined", 0.0),
                        raw.get("h1_alone", {}).get("h1_GBs", 0.0)) * 1e9
+        # the phase itself is a measurement of the host DRAM too: if it moved its
+        # bytes faster than every probe, the probes under-read the peak and the
+        # phase's own rate is the best lower bound on it (stated, never hidden)
+        dram_source = "best host-memory probe of this run (read / copy / H1, alone and next to duplex DMA)"
+        achieved_dram_Bps = host_bytes / (self.ms * 1e-3)
+        if achieved_dram_Bps > dram_Bps:
+            dram_Bps, dram_source = achieved_dram_Bps, "the phase itself (it moved host DRAM bytes faster than every probe)"
         h1_rate = raw.get("h1_alone", {}).get("h1_params_per_s", prof.cpu_update_params_per_s)
         link_dir_b = max(self.h2d_b, self.d2h_b + self.grads_d2h_b)
         bounds = {"hbm": BYTES_PER_PARAM_K1 * fast / (hbm_peak * 1e9),
@@ -681,7 +688,8 @@ class B200Bench:
                            "bound": "link" if bounds["link"] >= bounds["hbm"] else "hbm"},
             "link_GBs_per_dir_measured": link_Bps / 1e9, "host_dram_bytes_per_step": host_bytes,
             "host_dram_bytes_per_param": {"streamed": 24, "host_updated": cpu_host_B},
-            "host_dram_GBs_measured": dram_Bps / 1e9, "host_dram_probe": dram_probe,
+            "host_dram_GBs_measured": dram_Bps / 1e9, "host_dram_peak_source": dram_source,
+            "host_dram_GBs_achieved": achieved_dram_Bps / 1e9, "host_dram_probe": dram_probe,
             "host_update_ms_at_measured_rate": cpu / prof.cpu_update_params_per_s * 1e3,
             "grad_flush_in_phase": flush}
         spans = [r.measured.span_ns for r in self.results]

@@ -29,7 +29,7 @@ CXXFLAGS = [
     f"-I{CUDA_HOME / 'include'}", f"-I{INCLUDE}",
 ]
 ISA_FLAGS = {
-    "avx512": ["-mavx512f", "-mavx512bw", "-mavx512vl", "-mavx512dq", "-mprefer-vector-width=512"],
+    "avx512": ["-mavx512f", "-mavx512bw", "-mavx512vl", "-mavx512dq", "-mprfchw", "-mprefer-vector-width=512"],
     "avx2": ["-mavx2", "-mf16c"],
     "generic": [],
 }

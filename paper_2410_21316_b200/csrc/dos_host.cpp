@@ -187,6 +187,26 @@ void parallel_chunks(int64_t n, int nthreads, F&& body) {
     if (lo < hi) body(lo, hi);
   });
 }
+
+// Splits [0, n) into chunks of `chunk` elements (a multiple of 64) that the
+// team's threads claim from a shared counter: a thread that is preempted or
+// starved of memory bandwidth (the copy engines share the DRAM) costs the
+// section one chunk, not its whole static share.
+template <class F>
+void parallel_dynamic(int64_t n, int nthreads, int64_t chunk, F&& body) {
+  const std::shared_ptr<Team> hold = team();
+  Team& tm = *hold;
+  int k = nthreads > 0 ? std::min(nthreads, tm.size()) : tm.size();
+  k = (int)std::max<int64_t>(1, std::min<int64_t>(k, (n + chunk - 1) / chunk));
+  if (k <= 1) {
+    body((int64_t)0, n);
+    return;
+  }
+  std::atomic<int64_t> next{0};
+  tm.run(k, [&](int) {
+    for (int64_t c; (c = next.fetch_add(chunk, std::memory_order_relaxed)) < n;) body(c, std::min(n, c + chunk));
+  });
+}
 }  // namespace
 
 extern "C" int dos_host_threads(void) { return team()->size(); }
@@ -220,11 +240,37 @@ static bool h1_nt_all() {
   return c;
 }
 
+// DOS_H1_PF=<bytes>: write-intent prefetch distance of the default loop
+// (0: off).  DOS_H1_CHUNK=<elements>: H1's dynamic chunk (0: one static
+// contiguous share per thread).  Defaults from tools/h1_pf on the B200 boxes.
+static int64_t env_i64(const char* name, int64_t dflt) {
+  const char* e = getenv(name);
+  return e && *e ? (int64_t)strtoll(e, nullptr, 10) : dflt;
+}
+static int64_t h1_pf_bytes() {
+  static const int64_t v = std::max<int64_t>(0, env_i64("DOS_H1_PF", 1024));
+  return v;
+}
+static int64_t h1_chunk() {
+  static const int64_t v = [] {
+    const int64_t c = env_i64("DOS_H1_CHUNK", 1 << 18);
+    return c <= 0 ? (int64_t)0 : std::max<int64_t>(64, c & ~int64_t(63));
+  }();
+  return v;
+}
+
 int dos_host_adam(float* p, float* m, float* v, const void* g, int gt, void* lp, int lt, int64_t n,
                   const dos_kscal& s, int nthreads) {
   const dos_hk_table& t = hk();
-  const auto fn = h1_cached_w() ? t.adam_cached : h1_nt_all() ? t.adam_nta : t.adam;
-  parallel_chunks(n, nthreads, [&](int64_t lo, int64_t hi) { fn(p, m, v, g, gt, lp, lt, lo, hi, s); });
+  if (h1_cached_w() || h1_nt_all()) {
+    const auto fn = h1_cached_w() ? t.adam_cached : t.adam_nta;
+    parallel_chunks(n, nthreads, [&](int64_t lo, int64_t hi) { fn(p, m, v, g, gt, lp, lt, lo, hi, s); });
+    return DOS_OK;
+  }
+  const int64_t pf = h1_pf_bytes(), chunk = h1_chunk();
+  const auto body = [&](int64_t lo, int64_t hi) { t.adam_pf(p, m, v, g, gt, lp, lt, lo, hi, s, pf); };
+  if (chunk > 0) parallel_dynamic(n, nthreads, chunk, body);
+  else parallel_chunks(n, nthreads, body);
   return DOS_OK;
 }
 
@@ -365,6 +411,9 @@ extern "C" int dos_host_membw(const void* src, void* dst, size_t bytes, int mode
     const uint64_t* q = reinterpret_cast<const uint64_t*>(s);
     uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
     for (size_t i = 0; i + 4 <= n / 8; i += 4) {
+      // 1 KB ahead: without it one core keeps too few misses in flight and the
+      // pass measures per-core concurrency, not the DRAM (r02: 121 vs ~190 GB/s)
+      if ((i & 7) == 0) __builtin_prefetch(q + i + 128, 0, 3);
       a0 ^= q[i];
       a1 ^= q[i + 1];
       a2 ^= q[i + 2];

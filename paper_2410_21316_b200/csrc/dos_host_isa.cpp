@@ -17,4 +17,4 @@ namespace DOS_ISA_NS {
 
 extern const dos_hk_table DOS_CAT(dos_hk_, DOS_ISA_NS) = {DOS_ISA_NS::adam_range, DOS_ISA_NS::down_range,
                                                          DOS_ISA_NS::up_range, DOS_ISA_NS::adam_range_cached,
-                                                         DOS_ISA_NS::adam_range_nta};
+                                                         DOS_ISA_NS::adam_range_nta, DOS_ISA_NS::adam_range_pf};

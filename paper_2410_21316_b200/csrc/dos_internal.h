@@ -58,6 +58,7 @@ struct dos_hk_table {
   void (*up)(const void*, int, float*, int64_t, int64_t);
   void (*adam_cached)(float*, float*, float*, const void*, int, void*, int, int64_t, int64_t, const dos_kscal&);
   void (*adam_nta)(float*, float*, float*, const void*, int, void*, int, int64_t, int64_t, const dos_kscal&);
+  void (*adam_pf)(float*, float*, float*, const void*, int, void*, int, int64_t, int64_t, const dos_kscal&, int64_t);
 };
 
 // H1 through per-thread staging rings (the working copy of host-updated

@@ -43,6 +43,17 @@ def _torch():
 _LINK_BUFS: dict = {}  # nbytes -> probe buffers, allocated once per process and reused
 
 
+def _wait(*streams) -> None:
+    """Wait for ``streams`` on blocking-sync events: the waiting thread sleeps
+    instead of spinning on a core (a spinning probe thread steals a core from
+    the host team it runs next to and makes the team's static shares straggle)."""
+    torch = _torch()
+    for st in streams:
+        ev = torch.cuda.Event(blocking=True)
+        ev.record(st)
+        ev.synchronize()
+
+
 def _link_buffers(nbytes: int, numa_node: int = -1):
     """Pinned probe buffers of ``nbytes`` (pre-faulted huge pages, registered)
     and their device twins, allocated on first use and kept: a probe late in a
@@ -68,12 +79,12 @@ def measure_link(nbytes: int = 1 << 30, reps: int = 3, numa_node: int = -1) -> d
 
     def timed(fn) -> float:
         fn()
-        torch.cuda.synchronize()
+        _wait(s1, s2)
         best = float("inf")
         for _ in range(reps):
             t0 = time.perf_counter()
             fn()
-            torch.cuda.synchronize()
+            _wait(s1, s2)
             best = min(best, time.perf_counter() - t0)
         return best
 
@@ -187,8 +198,7 @@ def measure_h1(n: int = 100_000_000, with_dma: bool = False, reps: int = 3) -> d
                     dx.copy_(hx, non_blocking=True)
                 with torch.cuda.stream(s2):
                     hy.copy_(dy, non_blocking=True)
-                s1.synchronize()
-                s2.synchronize()
+                _wait(s1, s2)
                 moved[0] += 2 * nb
 
         dma = threading.Thread(target=pump, daemon=True)
@@ -196,7 +206,10 @@ def measure_h1(n: int = 100_000_000, with_dma: bool = False, reps: int = 3) -> d
         time.sleep(0.05)
     run = lambda: N.check(lib.dos_adam_step_host(p.ctypes.data, m.ctypes.data, v.ctypes.data, g.ctypes.data,
                                                   N.DOS_BF16, w.ctypes.data, N.DOS_BF16, n, sc, 0))
+    t0 = time.perf_counter()
     run()
+    if dma is not None:  # a window of >= 0.4 s, so the DMA byte count (64 MB grains) is fine enough
+        reps = max(reps, int(0.4 / max(1e-3, time.perf_counter() - t0)) + 1)
     best = float("inf")
     t_all0 = time.perf_counter()
     moved0 = moved[0] if dma is not None else 0
@@ -238,8 +251,7 @@ class _DuplexPump:
                 self.dx.copy_(self.hx, non_blocking=True)
             with torch.cuda.stream(self.s2):
                 self.hy.copy_(self.dy, non_blocking=True)
-            self.s1.synchronize()
-            self.s2.synchronize()
+            _wait(self.s1, self.s2)
             self.moved += 2 * self.nb
 
     def __enter__(self):

@@ -197,10 +197,12 @@ def test_team_resize_while_h1_runs():
     assert not th.is_alive() and not errors, errors
 
 
-@pytest.mark.parametrize("knob", ["DOS_H1_NT=all", "DOS_H1_WSTORE=cached"])
+@pytest.mark.parametrize("knob", ["DOS_H1_NT=all", "DOS_H1_WSTORE=cached", "DOS_H1_PF=0 DOS_H1_CHUNK=0",
+                                  "DOS_H1_PF=64 DOS_H1_CHUNK=64", "DOS_H1_PF=8192 DOS_H1_CHUNK=1000", ""])
 def test_host_store_variants_bit_exact(knob):
-    """The A/B store variants of H1 (streaming p/m/v stores; cached
-    working-copy stores) give the same bits, at aligned and misaligned starts."""
+    """The A/B variants of H1 (streaming p/m/v stores; cached working-copy
+    stores; prefetch distance and dynamic chunk, incl. chunks that split the
+    64-byte store phase) give the same bits, at aligned and misaligned starts."""
     import os
     import subprocess
     import sys
@@ -230,8 +232,8 @@ for n, off in ((1 << 20, 0), (300_001, 5), (4097, 17)):
     assert w[off:].tobytes() == O.lowp_from_f32(rp, "bf16").view(np.uint16).tobytes()
 print("ok")
 """
-    k, val = knob.split("=")
+    env = dict(os.environ, **dict(kv.split("=") for kv in knob.split()))
     root = Path(__file__).resolve().parent.parent
-    proc = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, **{k: val}),
+    proc = subprocess.run([sys.executable, "-c", code], cwd=root, env=env,
                           capture_output=True, text=True, timeout=300)
     assert proc.returncode == 0 and "ok" in proc.stdout, proc.stderr[-3000:]
