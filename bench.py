@@ -923,7 +923,10 @@ class B200Bench:
 
     def reference_schedule(self) -> None:
         """The reference's offload-to-CPU schedule (ALL_CPU blocking plan,
-        scheduler.py:301-319) executed by this runtime on the same box."""
+        scheduler.py:301-319) executed by this runtime on the same box, under
+        the same HBM budget as the run it is compared with: with no residents
+        (against the 0%-resident interleaved variant) and with the headline's
+        static residents (against the headline)."""
         if self.args.no_ref_schedule:
             self.out["reference_offload_schedule"] = None
             return
@@ -934,9 +937,22 @@ class B200Bench:
         rplan = D.build_plan(self.nsg, D.ALL_CPU)
         self.phase(rplan)
         ms = self.timed(lambda: self.phase(rplan), 2)
-        self.out["reference_offload_schedule"] = {
-            "ms_per_step": ms, "value": self.P / (ms * 1e-3), "speedup_of_headline": ms / self.ms,
-            "plan": "build_plan(N, ALL_CPU): CPU_UPDATE -> CPU_DOWNSCALE -> H2D_PARAMS16 chained"}
+        inter0 = next((v for v in self.out.get("static_variants") or []
+                       if v.get("static_ratio") == 0.0 and "ms_per_step" in v), None)
+        out = {"ms_per_step": ms, "value": self.P / (ms * 1e-3), "static_ratio": 0.0,
+               "speedup_of_interleaved_same_residency": (ms / inter0["ms_per_step"]) if inter0 else None,
+               "speedup_of_headline": ms / self.ms,
+               "plan": "build_plan(N, ALL_CPU): CPU_UPDATE -> CPU_DOWNSCALE -> H2D_PARAMS16 chained"}
+        if self.static_ratio > 0:
+            hplan = D.build_plan(self.nsg, D.ALL_CPU, static_ratio=self.static_ratio, placement=self.placement)
+            self.phase(hplan)
+            ms_h = self.timed(lambda: self.phase(hplan), 2)
+            out["at_headline_residency"] = {
+                "static_ratio": self.static_ratio, "ms_per_step": ms_h, "value": self.P / (ms_h * 1e-3),
+                "speedup_of_headline": ms_h / self.ms,
+                "plan": "build_plan(N, ALL_CPU, static_ratio): the same residents updated in HBM, every other "
+                        "subgroup CPU_UPDATE -> CPU_DOWNSCALE -> H2D_PARAMS16 chained"}
+        self.out["reference_offload_schedule"] = out
 
     # BASELINE.json configs with more than one rank: (total params, ranks)
     CONFIGS = {"13B/2": (13e9, 2), "20B/4": (20e9, 4), "20B/8": (20e9, 8), "70B/8": (70e9, 8)}
