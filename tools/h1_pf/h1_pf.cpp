@@ -4,6 +4,7 @@
 //   pfD    the same element math with prefetcht0 D bytes ahead on p, m, v, g
 //   pwD    prefetchw (read-for-ownership) D bytes ahead on p, m, v; prefetcht0 on g
 //   split2 each thread walks two halves of its slice alternately (8 read streams)
+//   pwdynD prefetchw D bytes ahead + 256K-element dynamic chunks (the shipped default)
 //   dynC   base loop over chunks of C elements handed out by an atomic counter
 //          (a late or preempted thread costs one chunk, not its whole slice)
 // Rates are taken over a >= 1 s window of back-to-back passes; the DMA bytes
@@ -150,6 +151,9 @@ int main(int argc, char** argv) {
         adam_pf<1>(p, m, v, g, w, lo, hi, s, atol(var.c_str() + 2));
       } else if (var.rfind("pw", 0) == 0) {
         adam_pf<2>(p, m, v, g, w, lo, hi, s, atol(var.c_str() + 2));
+      } else if (var.rfind("pwdyn", 0) == 0) {  // the shipped default: prefetchw D + 256K chunks
+        for (int64_t c; (c = next.fetch_add(1 << 18)) < n;)
+          adam_pf<2>(p, m, v, g, w, c, std::min(n, c + (1 << 18)), s, atol(var.c_str() + 5));
       } else if (var.rfind("dyn", 0) == 0) {
         const int64_t C = atol(var.c_str() + 3);
         for (int64_t c; (c = next.fetch_add(C)) < n;)
