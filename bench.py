@@ -638,9 +638,16 @@ class B200Bench:
             "peak_source": peak_source}
         # context: the same kernel alone on one 1e8-param subgroup (no concurrent
         # host-link DMA), CUDA events, median of 10
-        alone = self.profile_b200.measure_k1(self.SG, reps=10)
+        alone = self.profile_b200.measure_k1(self.SG, reps=10, with_dma=True)
         self.out["roofline"]["standalone"] = {"achieved": alone["k1_GBs"], "frac": alone["k1_GBs"] / hbm_peak,
                                               "ms_per_launch": alone["k1_ms"], "params": alone["n"]}
+        # the in-phase context: K1 and a plain device copy (the peak's own
+        # kernel) next to duplex host-link DMA — the copy's rate there is the
+        # HBM ceiling inside a phase; frac_of_copy = in-phase K1 against it
+        dma = alone["under_duplex_dma"]
+        self.out["roofline"]["under_duplex_dma"] = {
+            **dma, "copy_alone_GBs": alone["d2d_copy_GBs"], "copy_frac_of_peak": dma["d2d_copy_GBs"] / hbm_peak,
+            "in_phase_k1_frac_of_copy": (k1_gbs / dma["d2d_copy_GBs"]) if k1_gbs else None}
         # phase: HBM time of the fast-tier params, busier link direction at the
         # measured per-direction rate, host DRAM (24 B per streamed param of DMA;
         # 28 B per host-updated param of H1 + 2 B read by its H2D_PARAMS16 + 2 B

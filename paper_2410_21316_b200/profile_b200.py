@@ -133,8 +133,14 @@ def measure_link_under_h1(nbytes: int = 1 << 28, n: int = 50_000_000) -> dict:
     return res
 
 
-def measure_k1(n: int = 100_000_000, reps: int = 5) -> dict:
-    """K1 params/s and achieved HBM GB/s (28 B/param) on one subgroup."""
+def measure_k1(n: int = 100_000_000, reps: int = 5, with_dma: bool = False) -> dict:
+    """K1 params/s and achieved HBM GB/s (28 B/param) on one subgroup.
+
+    ``with_dma``: also K1 and a plain device-to-device copy (the HBM
+    roofline's own kernel) while duplex pinned DMA runs on two other streams,
+    as inside a phase: the copy's rate there is the HBM ceiling the in-phase
+    K1 can reach (host-link DMA costs HBM more than its own bytes;
+    profiles/r02_k1_variants_dma.jsonl)."""
     torch = _torch()
     dev = torch.device("cuda")
     p = torch.randn(n, device=dev) * 0.02
@@ -161,7 +167,33 @@ def measure_k1(n: int = 100_000_000, reps: int = 5) -> dict:
         e1.synchronize()
         times.append(e0.elapsed_time(e1) * 1e-3)
     t = float(np.median(times))
-    return {"k1_params_per_s": n / t, "k1_GBs": 28 * n / t / 1e9, "k1_ms": t * 1e3, "n": n}
+    out = {"k1_params_per_s": n / t, "k1_GBs": 28 * n / t / 1e9, "k1_ms": t * 1e3, "n": n}
+    if with_dma:
+        src = torch.empty(1 << 31, dtype=torch.uint8, device=dev)
+        dst = torch.empty_like(src)
+
+        def timed(fn) -> float:
+            fn()
+            ts = []
+            for _ in range(reps):
+                e0.record(st)
+                fn()
+                e1.record(st)
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1) * 1e-3)
+            return float(np.median(ts))
+
+        copy = lambda: dst.copy_(src)
+        out["d2d_copy_GBs"] = 2 * src.numel() / timed(copy) / 1e9
+        with _DuplexPump() as pump:
+            t0, m0 = time.perf_counter(), pump.moved
+            tk = timed(run)
+            tc = timed(copy)
+            dma = (pump.moved - m0) / (time.perf_counter() - t0)
+        out["under_duplex_dma"] = {"k1_GBs": 28 * n / tk / 1e9, "d2d_copy_GBs": 2 * src.numel() / tc / 1e9,
+                                   "dma_GBs": dma / 1e9}
+        del src, dst
+    return out
 
 
 def measure_h1(n: int = 100_000_000, with_dma: bool = False, reps: int = 3) -> dict:
