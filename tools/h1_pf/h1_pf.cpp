@@ -112,27 +112,38 @@ int main(int argc, char** argv) {
   const dos_kscal s = [&] { dos_kscal k{}; k.lr = sc.lr; k.b1 = sc.beta1; k.b2 = sc.beta2; k.eps = sc.eps;
     k.bc1 = sc.bc1; k.bc2 = sc.bc2; k.omb1 = 1.0f - k.b1; k.omb2 = 1.0f - k.b2; k.decay = 1.f; k.adamw = 0; return k; }();
 
-  // DMA pump
+  // DMA pump: DMA_H2D / DMA_D2H concurrent streams per direction (default 1
+  // each; more streams may land on more copy engines = more reads in flight)
   std::atomic<bool> stop{false};
-  std::atomic<uint64_t> moved{0};
+  std::atomic<uint64_t> moved{0}, moved_h2d{0}, moved_d2h{0};
   std::thread pump;
+  const int kh = getenv("DMA_H2D") ? atoi(getenv("DMA_H2D")) : 1;
+  const int kd = getenv("DMA_D2H") ? atoi(getenv("DMA_D2H")) : 1;
   if (dma) {
     const size_t nb = 64u << 20;
-    void *hx, *hy, *dx, *dy;
-    cudaHostAlloc(&hx, nb, 0); cudaHostAlloc(&hy, nb, 0); cudaMalloc(&dx, nb); cudaMalloc(&dy, nb);
-    memset(hx, 1, nb); memset(hy, 2, nb);
-    pump = std::thread([=, &stop, &moved] {
-      cudaStream_t a, b;
-      cudaEvent_t ea, eb;  // blocking-sync events: the pump sleeps, it does not spin on a core
-      cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking); cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking);
-      cudaEventCreateWithFlags(&ea, cudaEventBlockingSync | cudaEventDisableTiming);
-      cudaEventCreateWithFlags(&eb, cudaEventBlockingSync | cudaEventDisableTiming);
+    std::vector<void*> hs, ds;
+    for (int i = 0; i < kh + kd; ++i) {
+      void *h, *d;
+      cudaHostAlloc(&h, nb, 0); cudaMalloc(&d, nb); memset(h, 1 + i, nb);
+      hs.push_back(h); ds.push_back(d);
+    }
+    pump = std::thread([=, &stop, &moved, &moved_h2d, &moved_d2h] {
+      std::vector<cudaStream_t> st(kh + kd);
+      std::vector<cudaEvent_t> ev(kh + kd);  // blocking-sync events: the pump sleeps, it does not spin on a core
+      for (int i = 0; i < kh + kd; ++i) {
+        cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&ev[i], cudaEventBlockingSync | cudaEventDisableTiming);
+      }
       while (!stop.load()) {
-        cudaMemcpyAsync(dx, hx, nb, cudaMemcpyHostToDevice, a);
-        cudaMemcpyAsync(hy, dy, nb, cudaMemcpyDeviceToHost, b);
-        cudaEventRecord(ea, a); cudaEventRecord(eb, b);
-        cudaEventSynchronize(ea); cudaEventSynchronize(eb);
-        moved += 2 * nb;
+        for (int i = 0; i < kh + kd; ++i) {
+          if (i < kh) cudaMemcpyAsync(ds[i], hs[i], nb, cudaMemcpyHostToDevice, st[i]);
+          else cudaMemcpyAsync(hs[i], ds[i], nb, cudaMemcpyDeviceToHost, st[i]);
+          cudaEventRecord(ev[i], st[i]);
+        }
+        for (int i = 0; i < kh + kd; ++i) cudaEventSynchronize(ev[i]);
+        moved += (uint64_t)(kh + kd) * nb;
+        moved_h2d += (uint64_t)kh * nb;
+        moved_d2h += (uint64_t)kd * nb;
       }
     });
     std::this_thread::sleep_for(std::chrono::milliseconds(200));
@@ -145,7 +156,9 @@ int main(int argc, char** argv) {
       std::atomic<int64_t>& next = nexts[it];
       const int64_t per = ((n + T - 1) / T + 63) & ~int64_t(63);
       const int64_t lo = std::min<int64_t>(n, per * t), hi = std::min<int64_t>(n, lo + per);
-      if (var == "base") {
+      if (var == "idle") {  // no host work: the pump's rates alone
+        std::this_thread::sleep_for(std::chrono::milliseconds(50));
+      } else if (var == "base") {
         base::adam_range(p, m, v, g, DOS_BF16, w, DOS_BF16, lo, hi, s);
       } else if (var.rfind("pf", 0) == 0) {
         adam_pf<1>(p, m, v, g, w, lo, hi, s, atol(var.c_str() + 2));
@@ -177,7 +190,7 @@ int main(int argc, char** argv) {
     const int passes = std::max(2, std::min(4000, (int)(reps * 0.25 / best)));
     for (int i = 0; i < passes; ++i) nexts[i] = 0;
     std::atomic<int> arrived{0};
-    const uint64_t m0 = moved.load();
+    const uint64_t m0 = moved.load(), mh0 = moved_h2d.load(), md0 = moved_d2h.load();
     const double tsum = par(T, [&](int t) {
       for (int i = 0; i < passes; ++i) {
         pass(t, i);
@@ -187,10 +200,12 @@ int main(int argc, char** argv) {
     });
     const double win = tsum;
     const double dma_gbs = (moved.load() - m0) / win / 1e9;
+    const double h2d_gbs = (moved_h2d.load() - mh0) / win / 1e9, d2h_gbs = (moved_d2h.load() - md0) / win / 1e9;
     const double h1_rate = (double)n * passes / tsum;
     printf("{\"variant\": \"%s\", \"threads\": %d, \"dma\": %d, \"h1_Gparams_s\": %.3f, \"h1_best_Gparams_s\": %.3f, "
-           "\"h1_GBs\": %.1f, \"dma_GBs\": %.1f, \"combined_GBs\": %.1f, \"passes\": %d, \"bitexact_vs_base\": %s}\n",
-           var.c_str(), T, dma, h1_rate / 1e9, n / best / 1e9, 28.0 * h1_rate / 1e9, dma_gbs,
+           "\"h1_GBs\": %.1f, \"dma_GBs\": %.1f, \"h2d_streams\": %d, \"d2h_streams\": %d, \"h2d_GBs\": %.1f, "
+           "\"d2h_GBs\": %.1f, \"combined_GBs\": %.1f, \"passes\": %d, \"bitexact_vs_base\": %s}\n",
+           var.c_str(), T, dma, h1_rate / 1e9, n / best / 1e9, 28.0 * h1_rate / 1e9, dma_gbs, kh, kd, h2d_gbs, d2h_gbs,
            28.0 * h1_rate / 1e9 * (tsum / win) + dma_gbs, passes, (var == "base" || same) ? "true" : "false");
     fflush(stdout);
   }
