@@ -74,6 +74,9 @@ def parse():
                          "includes their in-phase D2H flush by default)")
     ap.add_argument("--host-threads", type=int, default=0, help="H1 team size (0: all allowed cores / ranks)")
     ap.add_argument("--trace-dir", default=None, help="write measured/predicted timelines as trace CSVs")
+    ap.add_argument("--numa", default="gpu", choices=["gpu", "all"],
+                    help="host cores and pinned pool: 'gpu' = the GPU's NUMA node (each rank's share of it at N>1; "
+                         "a no-op on a one-node host), 'all' = every allowed core, pool first-touched by the team (N=1)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N>1 (gloo: dry run with ranks sharing GPUs)")
     ap.add_argument("--no-ref-schedule", action="store_true",
@@ -427,14 +430,14 @@ class B200Bench:
                 dist.init_process_group("nccl", device_id=self.device)
             else:
                 dist.init_process_group("gloo")
-            # each rank's H1 team on its own share of the host cores (its GPU's NUMA node)
-            from paper_2410_21316_b200.distributed import bind_host_cores
+        # each rank's H1 team on its own share of the host cores (its GPU's NUMA
+        # node; at N=1 the whole node), and the pinned pool bound to that node
+        from paper_2410_21316_b200.distributed import bind_host_cores, gpu_numa_node
 
+        self.numa = -1
+        if world > 1 or args.numa == "gpu":
             self.cores = bind_host_cores(local, int(os.environ.get("LOCAL_WORLD_SIZE", world)))
-        # the pinned pool on the GPU's NUMA node (first touch by the rank's own team otherwise)
-        from paper_2410_21316_b200.distributed import gpu_numa_node
-
-        self.numa = gpu_numa_node(dev_index) if world > 1 else -1
+            self.numa = gpu_numa_node(dev_index)
         if args.host_threads > 0:
             D._native.lib().dos_set_host_threads(args.host_threads)
         self.P, self.SG = int(args.params), int(args.subgroup)
@@ -1138,6 +1141,8 @@ class B200Bench:
                 "data": "synthetic (seeded, generated on device)", "config": config}
         line.update(self.out)
         line["host"] = host_facts(self.device.index)
+        line["host"]["binding"] = {"numa": self.args.numa, "pool_numa_node": self.numa,
+                                   "h1_cpus": len(getattr(self, "cores", None) or os.sched_getaffinity(0))}
         line["profile"] = {"channel_params_per_s": prof.channel_params_per_s,
                            "fast_update_params_per_s": prof.fast_update_params_per_s,
                            "cpu_update_params_per_s": prof.cpu_update_params_per_s,

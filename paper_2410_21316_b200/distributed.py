@@ -362,11 +362,14 @@ def plan_core_binding(allowed, gpu_nodes, node_cpus, local_rank: int) -> list[in
     ``node_cpus[node]``: that node's CPUs.  Ranks whose GPUs sit on the same
     node split that node's allowed CPUs into equal contiguous slices (the
     paper pins each rank's CPU optimizer work to its socket, §8(e)); without
-    NUMA information the allowed CPUs are split evenly across all ranks."""
+    NUMA information the allowed CPUs are split evenly across all ranks.  A
+    single rank keeps its GPU's node (all allowed CPUs when that is unknown)."""
     allowed = sorted(set(allowed))
     world = len(gpu_nodes)
     if world <= 1:
-        return allowed
+        node = gpu_nodes[0] if world else -1
+        mine = [c for c in allowed if c in set(node_cpus.get(node, ()))] if node >= 0 else []
+        return mine or allowed
     node = gpu_nodes[local_rank]
     pool = [c for c in allowed if c in set(node_cpus.get(node, ()))] if node >= 0 else []
     peers = [r for r in range(world) if gpu_nodes[r] == node] if pool else list(range(world))

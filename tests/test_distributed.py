@@ -171,5 +171,8 @@ def test_plan_core_binding():
     # fewer cores than ranks, and a single rank keeps everything
     assert plan_core_binding([0, 1], [-1] * 4, {}, 3) == [1]
     assert plan_core_binding(range(8), [0], nodes, 0) == list(range(8))
+    # a single rank on a two-socket host keeps its GPU's socket; unknown node: everything
+    assert plan_core_binding(allowed, [1], nodes, 0) == list(range(16, 32))
+    assert plan_core_binding(allowed, [-1], nodes, 0) == list(range(32))
     # a node whose CPUs are outside the allowed mask falls back to the mask
     assert plan_core_binding(range(4), [2, 2], {2: [40, 41]}, 1) == [2, 3]
