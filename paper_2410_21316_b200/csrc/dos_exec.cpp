@@ -89,6 +89,24 @@ const GRingCfg& gring_cfg() {
   return c;
 }
 
+// Split copies (A/B knob, off by default): each H2D-lane copy of a subgroup
+// (PREFETCH_M/V/P, H2D_PARAMS16) — and with DOS_D2H_SPLIT each FLUSH_OUT_* —
+// goes out as k pieces on k streams (the lane's own + k-1 helpers forked and
+// joined by events), so more copy engines keep host reads in flight while the
+// host team loads the DRAM.  The action still ends when its last piece has.
+int split_env(const char* name) {
+  const char* e = getenv(name);
+  return e ? std::max(1, std::min(8, atoi(e))) : 1;
+}
+int h2d_split() {
+  static const int k = split_env("DOS_H2D_SPLIT");
+  return k;
+}
+int d2h_split() {
+  static const int k = split_env("DOS_D2H_SPLIT");
+  return k;
+}
+
 const RingCfg& ring_cfg() {
   static RingCfg c = [] {
     RingCfg r{false, 4, 1 << 16, 16};  // per thread 4 x 64K elements (512 KB of bf16: the core's L2)
@@ -128,6 +146,8 @@ struct Engine {
   cudaStream_t gst = nullptr;                        // in-phase grad flush (D2H); host_io: residents' grads H2D
   cudaStream_t ost = nullptr;                        // host_io: residents' working copy D2H
   cudaStream_t pst = nullptr;                        // fused all-gather: host subgroups' peer forwards
+  cudaStream_t hst[2][7] = {};                       // split-copy helpers of the h2d / d2h lanes
+  cudaEvent_t sev_fork[2] = {}, sev_join[2][7] = {};
   cudaStream_t wst = nullptr;                        // the shuttle kernel's stream
   // staging ring (see RingCfg) served by the shuttle kernel; ring_phase: used in this phase
   bool ring_phase = false;
@@ -550,6 +570,36 @@ struct Engine {
                            (size_t)n * 2, cudaMemcpyDeviceToHost, s);
   }
 
+  // One lane copy as k pieces on the lane stream + k-1 helpers (see h2d_split).
+  int lane_copy(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t s) {
+    const int dir = kind == cudaMemcpyHostToDevice ? 0 : 1;
+    const int k = dir == 0 ? h2d_split() : d2h_split();
+    const size_t piece = ((bytes + k - 1) / k + 4095) & ~size_t(4095);
+    if (k == 1 || bytes < 2 * piece) {
+      DOS_CU(cudaMemcpyAsync(dst, src, bytes, kind, s));
+      return DOS_OK;
+    }
+    if (!sev_fork[dir]) {
+      DOS_CU(cudaEventCreateWithFlags(&sev_fork[dir], cudaEventDisableTiming));
+      for (int h = 0; h < 7; ++h) {
+        DOS_CU(cudaStreamCreateWithFlags(&hst[dir][h], cudaStreamNonBlocking));
+        DOS_CU(cudaEventCreateWithFlags(&sev_join[dir][h], cudaEventDisableTiming));
+      }
+    }
+    DOS_CU(cudaEventRecord(sev_fork[dir], s));
+    int h = 0;
+    for (size_t off = piece; off < bytes; off += piece, ++h) {
+      const size_t n = std::min(piece, bytes - off);
+      DOS_CU(cudaStreamWaitEvent(hst[dir][h], sev_fork[dir], 0));
+      DOS_CU(cudaMemcpyAsync(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, n, kind,
+                             hst[dir][h]));
+      DOS_CU(cudaEventRecord(sev_join[dir][h], hst[dir][h]));
+    }
+    DOS_CU(cudaMemcpyAsync(dst, src, std::min(piece, bytes), kind, s));
+    for (int i = 0; i < h; ++i) DOS_CU(cudaStreamWaitEvent(s, sev_join[dir][i], 0));
+    return DOS_OK;
+  }
+
   int enqueue_gpu(const dos_action_desc* a, cudaStream_t s) {
     const int sg = a->subgroup;
     const int64_t start = sg_start[sg], n = sg_size[sg];
@@ -568,7 +618,8 @@ struct Engine {
           return dos_set_error(DOS_ESTATE, "subgroup %d piece %c staged twice", sg, "mvp"[piece]);
         sg_mask[sg] |= (uint8_t)(1u << piece);
         const float* src = (piece == PIECE_M ? S.host_m : piece == PIECE_V ? S.host_v : S.host_p) + start;
-        DOS_CU(cudaMemcpyAsync(slot_ptr(sg_slot[sg], piece), src, (size_t)n * 4, cudaMemcpyHostToDevice, s));
+        if (const int rc = lane_copy(slot_ptr(sg_slot[sg], piece), src, (size_t)n * 4, cudaMemcpyHostToDevice, s))
+          return rc;
         if (S.host_io && piece == PIECE_P) DOS_CU(copy_grads_h2d(start, n, s));
         return DOS_OK;
       }
@@ -627,7 +678,7 @@ struct Engine {
           return dos_set_error(DOS_ESTATE, "subgroup %d piece %c not resident on device", sg, "mvp"[piece]);
         float* dst = (piece == PIECE_M ? S.host_m : piece == PIECE_V ? S.host_v : S.host_p) + start;
         const int sl = sg_slot[sg];
-        DOS_CU(cudaMemcpyAsync(dst, slot_ptr(sl, piece), (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+        if (const int rc = lane_copy(dst, slot_ptr(sl, piece), (size_t)n * 4, cudaMemcpyDeviceToHost, s)) return rc;
         if (S.host_io && piece == PIECE_P) DOS_CU(copy_lowp_d2h(start, n, s));
         sg_mask[sg] &= (uint8_t)~(1u << piece);
         if (sg_mask[sg] == 0) {  // window closes with this flush
@@ -643,8 +694,9 @@ struct Engine {
           if (wait_fn((CUstream)s, ring_flags_dev + 4 * (CUdeviceptr)sg, epoch, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
             return dos_set_error(DOS_ECUDA, "cuStreamWaitValue32 (staging ring) failed");
         } else {
-          DOS_CU(cudaMemcpyAsync(dev_lowp + 2 * start, static_cast<const char*>(S.host_lowp) + 2 * start, (size_t)n * 2,
-                                 cudaMemcpyHostToDevice, s));
+          if (const int rc = lane_copy(dev_lowp + 2 * start, static_cast<const char*>(S.host_lowp) + 2 * start,
+                                       (size_t)n * 2, cudaMemcpyHostToDevice, s))
+            return rc;
         }
         // fused all-gather for a host subgroup: forward it peer-to-peer (NVLink
         // copy engines) on the peer stream, chained by event, so the next
@@ -934,6 +986,16 @@ struct Engine {
         cudaStreamSynchronize(side);
         cudaStreamDestroy(side);
       }
+    for (int d = 0; d < 2; ++d) {
+      for (int h = 0; h < 7; ++h) {
+        if (hst[d][h]) {
+          cudaStreamSynchronize(hst[d][h]);
+          cudaStreamDestroy(hst[d][h]);
+        }
+        if (sev_join[d][h]) cudaEventDestroy(sev_join[d][h]);
+      }
+      if (sev_fork[d]) cudaEventDestroy(sev_fork[d]);
+    }
     for (auto e : ev_s) cudaEventDestroy(e);
     for (auto e : ev_e) cudaEventDestroy(e);
     for (auto e : ev_g) cudaEventDestroy(e);
