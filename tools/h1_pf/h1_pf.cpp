@@ -25,6 +25,8 @@
 
 #include "../../paper_2410_21316_b200/csrc/dos_internal.h"
 
+extern "C" int zc_copy(int push, const void* src, void* dst, size_t bytes, int ctas, cudaStream_t st);
+
 namespace base {
 #include "../../paper_2410_21316_b200/csrc/dos_host_kern.inc"
 }
@@ -119,7 +121,35 @@ int main(int argc, char** argv) {
   std::thread pump;
   const int kh = getenv("DMA_H2D") ? atoi(getenv("DMA_H2D")) : 1;
   const int kd = getenv("DMA_D2H") ? atoi(getenv("DMA_D2H")) : 1;
-  if (dma) {
+  // DMA_PULL=<ctas>: the H2D direction by SM zero-copy loads instead of the
+  // copy engines; DMA_PUSH=<ctas>: the D2H direction by SM stores
+  const int pull = getenv("DMA_PULL") ? atoi(getenv("DMA_PULL")) : 0;
+  const int push = getenv("DMA_PUSH") ? atoi(getenv("DMA_PUSH")) : 0;
+  if (dma && (pull || push)) {
+    const size_t nb = 64u << 20;
+    void *hx, *hy, *hxd, *hyd, *dx, *dy;
+    cudaHostAlloc(&hx, nb, cudaHostAllocMapped); cudaHostAlloc(&hy, nb, cudaHostAllocMapped);
+    cudaHostGetDevicePointer(&hxd, hx, 0); cudaHostGetDevicePointer(&hyd, hy, 0);
+    cudaMalloc(&dx, nb); cudaMalloc(&dy, nb);
+    memset(hx, 1, nb); memset(hy, 2, nb);
+    pump = std::thread([=, &stop, &moved, &moved_h2d, &moved_d2h] {
+      cudaStream_t a, b;
+      cudaEvent_t ea, eb;
+      cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking); cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&ea, cudaEventBlockingSync | cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&eb, cudaEventBlockingSync | cudaEventDisableTiming);
+      while (!stop.load()) {
+        if (pull) zc_copy(0, hxd, dx, nb, pull, a);
+        else cudaMemcpyAsync(dx, hx, nb, cudaMemcpyHostToDevice, a);
+        if (push) zc_copy(1, dy, hyd, nb, push, b);
+        else cudaMemcpyAsync(hy, dy, nb, cudaMemcpyDeviceToHost, b);
+        cudaEventRecord(ea, a); cudaEventRecord(eb, b);
+        cudaEventSynchronize(ea); cudaEventSynchronize(eb);
+        moved += 2 * nb; moved_h2d += nb; moved_d2h += nb;
+      }
+    });
+    std::this_thread::sleep_for(std::chrono::milliseconds(200));
+  } else if (dma) {
     const size_t nb = 64u << 20;
     std::vector<void*> hs, ds;
     for (int i = 0; i < kh + kd; ++i) {
