@@ -100,6 +100,26 @@ def test_two_rank_zero3_step_matches_oracle(stride, fused, fused_reduce, average
     assert all(ok for _, ok, _ in res), res
 
 
+@pytest.mark.parametrize("stride,fused,fused_reduce,average", [
+    (2, True, True, False), (3, True, True, True), (2, False, False, False)])
+def test_four_rank_zero3_step_matches_oracle(stride, fused, fused_reduce, average):
+    """Four ranks on the one B200: three IPC peers per rank, the local tile at
+    every position of the rank-order sum (ranks 1 and 2 sit in the middle)."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, 4, port, stride, fused, q, fused_reduce, average, 0.2))
+             for r in range(4)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=400) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok, _ in res), res
+
+
 def _resume_worker(rank, world, port, q):
     try:
         import torch.distributed as dist
