@@ -509,9 +509,14 @@ class B200Bench:
         self.P_rank = sum(g.size for g in mine)
         self.sizes = [g.size for g in mine]
         self.nsg = len(self.sizes)
+        # the link's peak, probed on a quiet box with buffers allocated before
+        # the pool (and reused by the later re-probe, copy_streams); before the
+        # capacity-aware budget below, which must see them as used
+        self.link_setup = self.profile_b200.measure_link(1 << 30, numa_node=self.numa)
         if a.static_ratio == "auto":
             # capacity-aware residency: as many subgroups homed in HBM as fit
             # beside the grads, the working copy and two windows
+            torch.cuda.empty_cache()
             free = torch.cuda.mem_get_info(self.device)[0]
             ratio = self.policy.capacity_static_ratio(self.sizes, free)
             self.static_ratio = -self.max_over_ranks(-ratio)  # same plan shape on every rank
@@ -519,9 +524,6 @@ class B200Bench:
             self.static_ratio = float(a.static_ratio)
         self.placement = D.Placement(a.placement)
         static = D.build_plan(self.nsg, 1, static_ratio=self.static_ratio, placement=self.placement).static_set
-        # the link's peak, probed on a quiet box with buffers allocated before
-        # the pool (and reused by the later re-probe, copy_streams)
-        self.link_setup = self.profile_b200.measure_link(1 << 30, numa_node=self.numa)
         t0 = time.perf_counter()
         # sparse pinned pool: host memory only for the host-homed subgroups
         self.opt = D.ShardedOptimizer.allocate(self.P_rank, self.SG, lowp=a.lowp, numa_node=self.numa,
@@ -535,6 +537,7 @@ class B200Bench:
         cap = None if self.args.capacity_gb is None else int(self.args.capacity_gb * 1e9)
         self.cap = cap
         self.profile = self.profile_b200.measure_profile(fast_capacity_bytes=cap, quick=True)
+        torch.cuda.empty_cache()  # the probes' cached blocks: the engine's windows are plain cudaMalloc
 
     def choose_plan(self) -> None:
         """Reference planner's choice for one calibration step, re-fit, then
@@ -647,8 +650,8 @@ class B200Bench:
         # the in-phase context: K1 and a plain device copy (the peak's own
         # kernel) next to duplex host-link DMA — the copy's rate there is the
         # HBM ceiling inside a phase; frac_of_copy = in-phase K1 against it
-        dma = alone["under_duplex_dma"]
-        self.out["roofline"]["under_duplex_dma"] = {
+        dma = alone.get("under_duplex_dma")
+        self.out["roofline"]["under_duplex_dma"] = alone.get("under_duplex_dma_skipped") if dma is None else {
             **dma, "copy_alone_GBs": alone["d2d_copy_GBs"], "copy_frac_of_peak": dma["d2d_copy_GBs"] / hbm_peak,
             "in_phase_k1_frac_of_copy": (k1_gbs / dma["d2d_copy_GBs"]) if k1_gbs else None}
         # phase: HBM time of the fast-tier params, busier link direction at the

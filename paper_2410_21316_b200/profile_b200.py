@@ -55,19 +55,19 @@ def _wait(*streams) -> None:
 
 
 def _link_buffers(nbytes: int, numa_node: int = -1):
-    """Pinned probe buffers of ``nbytes`` (pre-faulted huge pages, registered)
-    and their device twins, allocated on first use and kept: a probe late in a
-    run reuses the pages it got at start-up instead of fresh ones from a
-    fragmented host (which measured the link 30-40% low in round 1)."""
+    """Pinned probe buffers of ``nbytes`` (pre-faulted huge pages, registered),
+    allocated on first use and kept: a probe late in a run reuses the pages it
+    got at start-up instead of fresh ones from a fragmented host (which
+    measured the link 30-40% low in round 1).  The device twins are made per
+    probe and freed after it, so they never hold HBM a capacity-aware
+    residency could use."""
     torch = _torch()
     key = (nbytes, numa_node, torch.cuda.current_device())
     if key not in _LINK_BUFS:
         hb1, hb2 = N.HostBuffer(nbytes, numa_node=numa_node), N.HostBuffer(nbytes, numa_node=numa_node)
         h1 = torch.from_numpy(hb1.array(np.uint8, nbytes))
         h2 = torch.from_numpy(hb2.array(np.uint8, nbytes))
-        d1 = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
-        d2 = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
-        _LINK_BUFS[key] = (hb1, hb2, h1, h2, d1, d2, torch.cuda.Stream(), torch.cuda.Stream())
+        _LINK_BUFS[key] = (hb1, hb2, h1, h2, torch.cuda.Stream(), torch.cuda.Stream())
     return _LINK_BUFS[key]
 
 
@@ -75,7 +75,9 @@ def measure_link(nbytes: int = 1 << 30, reps: int = 3, numa_node: int = -1) -> d
     """Pinned host<->device GB/s: each direction alone and both at once
     (best of ``reps``; buffers reused across calls, see ``_link_buffers``)."""
     torch = _torch()
-    _, _, h1, h2, d1, d2, s1, s2 = _link_buffers(nbytes, numa_node)
+    _, _, h1, h2, s1, s2 = _link_buffers(nbytes, numa_node)
+    d1 = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
 
     def timed(fn) -> float:
         fn()
@@ -99,6 +101,8 @@ def measure_link(nbytes: int = 1 << 30, reps: int = 3, numa_node: int = -1) -> d
     t_h2d = timed(h2d)
     t_d2h = timed(d2h)
     t_dup = timed(lambda: (h2d(), d2h()))
+    del d1, d2  # every copy has finished (timed() waits on both streams)
+    torch.cuda.empty_cache()
     return {"h2d_GBs": nbytes / t_h2d / 1e9, "d2h_GBs": nbytes / t_d2h / 1e9,
             "duplex_GBs_per_dir": nbytes / t_dup / 1e9}
 
@@ -169,7 +173,12 @@ def measure_k1(n: int = 100_000_000, reps: int = 5, with_dma: bool = False) -> d
     t = float(np.median(times))
     out = {"k1_params_per_s": n / t, "k1_GBs": 28 * n / t / 1e9, "k1_ms": t * 1e3, "n": n}
     if with_dma:
-        src = torch.empty(1 << 31, dtype=torch.uint8, device=dev)
+        # 2 GB each way, less when the HBM is mostly taken (capacity-aware residency)
+        nb = min(1 << 31, (torch.cuda.mem_get_info(dev)[0] - (2 << 30)) // 2) & ~((1 << 20) - 1)
+        if nb < (256 << 20):
+            out["under_duplex_dma_skipped"] = {"skipped": "no HBM left for the device-copy buffers"}
+            return out
+        src = torch.empty(nb, dtype=torch.uint8, device=dev)
         dst = torch.empty_like(src)
 
         def timed(fn) -> float:
@@ -193,6 +202,7 @@ def measure_k1(n: int = 100_000_000, reps: int = 5, with_dma: bool = False) -> d
         out["under_duplex_dma"] = {"k1_GBs": 28 * n / tk / 1e9, "d2d_copy_GBs": 2 * src.numel() / tc / 1e9,
                                    "dma_GBs": dma / 1e9}
         del src, dst
+        torch.cuda.empty_cache()
     return out
 
 
