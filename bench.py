@@ -785,7 +785,8 @@ class B200Bench:
             "h2d_bytes_per_step": (2 * fast + h2d_b) * self.world,
             "d2h_bytes_per_step": (2 * fast + d2h_b) * self.world, "ms_per_step": ms,
             "api": "execute_plan(..., host_io=True): grads from pinned host, working copy back to host",
-            "host_resident_params": (self.P_rank - fast) * self.world, "stride": plan.stride,
+            "host_resident_params": (self.P_rank - fast) * self.world,
+            "stride": "all_cpu" if plan.stride is D.ALL_CPU else plan.stride,
             "measured_ms_by_stride": tried}
 
     def collectives(self) -> None:
@@ -1168,7 +1169,8 @@ class B200Bench:
         self.traces()
         self.baseline_configs()
         if self.rank == 0:
-            print(json.dumps(self.line()), flush=True)
+            # default=str: any plan sentinel (ALL_CPU) that reaches the line prints by name
+            print(json.dumps(self.line(), default=str), flush=True)
         if self.world > 1:
             self.dist.destroy_process_group()
 
